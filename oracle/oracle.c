@@ -1,0 +1,172 @@
+/*
+ * oracle.c -- plain, slow, sequential CPU oracle for the GTaP hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY. Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load this library.
+ * The product path (paper_2604_05982_b200/, include/gtap.h) never links,
+ * imports or calls it, and this file shares no code, header, table or
+ * constant with the CUDA path.
+ *
+ * Every function restates what the paper (reference/PAPER.md, cited "P:n" =
+ * line n) defines, written the obvious way: plain recursion, plain loops,
+ * fp64 accumulation where the paper leaves floating point open. Readings of
+ * ambiguous passages are the ones listed in DESIGN.md "Readings".
+ *
+ * Pins (tests/test_oracle_*.py, -m "not gpu"):
+ *   fib        -- iterative F(n), OEIS/SPEC values, closed-form call counts
+ *   mergesort  -- numpy sort, exhaustive permutations, closed-form task count
+ *   spmv       -- dense fp64 matmul on tiny matrices, identity / ones rows
+ *   bfs        -- all-pairs shortest paths (scipy) on every 5-vertex graph,
+ *                 Graph500-style validity on RMAT graphs
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ------------------------------------------------------------------ fib */
+/*
+ * P:1023-1033 (Prog. fib, §5.1.2):
+ *     if (n < 2) return n;  a = fib(n-1);  b = fib(n-2);  taskwait;  return a+b;
+ * Every call is one task ("we disable the cutoff and spawn a task at every
+ * recursive call"). Invocations follow the transformed state machine
+ * (P:1168-1190): a call with n < 2 finishes in case 0 (1 invocation); any
+ * other call runs case 0 (spawn + prepare_for_join) and case 1 (load the two
+ * child results, finish) -- 2 invocations.
+ */
+static int64_t fib_rec(int32_t n, int64_t *calls, int64_t *invocations)
+{
+    *calls += 1;
+    if (n < 2) {
+        *invocations += 1;
+        return n;
+    }
+    int64_t a = fib_rec(n - 1, calls, invocations);
+    int64_t b = fib_rec(n - 2, calls, invocations);
+    *invocations += 2;
+    return a + b;
+}
+
+int oracle_fib(int32_t n, int64_t *value, int64_t *calls, int64_t *invocations)
+{
+    if (n < 0 || n > 92) return -1;
+    *calls = 0;
+    *invocations = 0;
+    *value = fib_rec(n, calls, invocations);
+    return 0;
+}
+
+/* ------------------------------------------------------------ mergesort */
+/*
+ * P:153-165 (Prog. cutoff mergesort, §4.4) with the state machine of
+ * P:59-74 (§4.2):
+ *     if (right - left <= CUTOFF) { sequential_sort(data, left, right); return; }
+ *     mid = (left + right) / 2;  fork ms(left, mid);  fork ms(mid, right);
+ *     join;  merge(data, left, mid, right);
+ * Readings (R14, R15): half-open [l, r); mid = l + (r - l) / 2;
+ * sequential_sort = insertion sort; merge = two-pointer merge into scratch
+ * taking the left element on ties, then copy back.
+ * Tasks = calls; invocations: a leaf runs once, an internal node twice
+ * (case 0 spawns, case 1 merges).
+ */
+static void insertion_sort(int32_t *a, int64_t l, int64_t r)
+{
+    for (int64_t i = l + 1; i < r; i++) {
+        int32_t v = a[i];
+        int64_t j = i - 1;
+        while (j >= l && a[j] > v) {
+            a[j + 1] = a[j];
+            j--;
+        }
+        a[j + 1] = v;
+    }
+}
+
+static void merge_runs(int32_t *a, int32_t *tmp, int64_t l, int64_t m, int64_t r)
+{
+    int64_t i = l, j = m, k = l;
+    while (i < m && j < r) {
+        if (a[j] < a[i]) tmp[k++] = a[j++];
+        else             tmp[k++] = a[i++];
+    }
+    while (i < m) tmp[k++] = a[i++];
+    while (j < r) tmp[k++] = a[j++];
+    memcpy(a + l, tmp + l, (size_t)(r - l) * sizeof(int32_t));
+}
+
+static void ms_rec(int32_t *a, int32_t *tmp, int64_t l, int64_t r, int64_t cutoff,
+                   int64_t *tasks, int64_t *invocations)
+{
+    *tasks += 1;
+    if (r - l <= cutoff) {
+        insertion_sort(a, l, r);
+        *invocations += 1;
+        return;
+    }
+    int64_t m = l + (r - l) / 2;
+    ms_rec(a, tmp, l, m, cutoff, tasks, invocations);
+    ms_rec(a, tmp, m, r, cutoff, tasks, invocations);
+    merge_runs(a, tmp, l, m, r);
+    *invocations += 2;
+}
+
+int oracle_mergesort(int32_t *data, int32_t *scratch, int64_t n, int64_t cutoff,
+                     int64_t *tasks, int64_t *invocations)
+{
+    if (n < 0 || cutoff < 1) return -1;
+    *tasks = 0;
+    *invocations = 0;
+    ms_rec(data, scratch, 0, n, cutoff, tasks, invocations);
+    return 0;
+}
+
+/* ----------------------------------------------------------------- SpMV */
+/*
+ * SpMV is only named by the paper as a block-cooperative workload (P:42,
+ * §4.1); its definition is the standard CSR product
+ *     y[i] = sum_{j = row_ptr[i]}^{row_ptr[i+1]-1} val[j] * x[col[j]],
+ * accumulated here in fp64 and rounded once (R21).
+ */
+int oracle_spmv(const int32_t *row_ptr, const int32_t *col, const float *val,
+                const float *x, int64_t nrows, double *y64, float *y32)
+{
+    for (int64_t i = 0; i < nrows; i++) {
+        double s = 0.0;
+        for (int64_t j = row_ptr[i]; j < row_ptr[i + 1]; j++)
+            s += (double)val[j] * (double)x[col[j]];
+        if (y64) y64[i] = s;
+        if (y32) y32[i] = (float)s;
+    }
+    return 0;
+}
+
+/* ------------------------------------------------------------------ BFS */
+/*
+ * P:1053-1068 (Prog. graph traversal, §5.1.3) relaxes depth[u] with
+ * atomicMin(depth[u], depth[v] + 1) and spawns bfs(u) on improvement, from
+ * depth[src] = 0. At quiescence this is the unweighted shortest-path
+ * distance (proof sketch in tests/test_oracle_bfs.py), so the oracle is the
+ * textbook FIFO breadth-first search. Unreached vertices keep INT32_MAX.
+ */
+int oracle_bfs(const int32_t *row_ptr, const int32_t *col, int64_t nv, int32_t src,
+               int32_t *depth)
+{
+    if (src < 0 || src >= nv) return -1;
+    int32_t *queue = (int32_t *)malloc((size_t)(nv > 0 ? nv : 1) * sizeof(int32_t));
+    if (!queue) return -2;
+    for (int64_t v = 0; v < nv; v++) depth[v] = INT32_MAX;
+    int64_t qh = 0, qt = 0;
+    depth[src] = 0;
+    queue[qt++] = src;
+    while (qh < qt) {
+        int32_t v = queue[qh++];
+        for (int64_t e = row_ptr[v]; e < row_ptr[v + 1]; e++) {
+            int32_t u = col[e];
+            if (depth[u] == INT32_MAX) {
+                depth[u] = depth[v] + 1;
+                queue[qt++] = u;
+            }
+        }
+    }
+    free(queue);
+    return 0;
+}

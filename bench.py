@@ -1,0 +1,458 @@
+#!/usr/bin/env python3
+"""Benchmark of the GTaP hot path on B200 (driver contract: one JSON line on rank 0).
+
+Workload (N=1): BASELINE.json configs[1] -- mergesort of 2^24 random int32 keys,
+thread-level fork-join with cutoff 128, metric
+Mkeys/s. A "step" is one run of the persistent scheduler over a fresh copy of
+the keys: root spawn + the persistent kernel (init and result retrieval are
+excluded, as in the paper). Between steps (untimed) the keys are
+restored, L2 is flushed by writing a 256 MiB buffer, and gtap_reset re-arms
+the workspace. Each step is timed with CUDA events on the launching stream.
+
+Secondary results in the same line (`secondary`): fib(40) tasks/s
+(configs[2]) against the measured L2-atomic rate, SpMV (configs[3]) GB/s
+against HBM, BFS RMAT-22 (configs[4]) GTEPS. Multi-GPU (torchrun): every rank
+runs an independent replica of the workload (weak scaling, no collective on
+the data path); one all_gather of per-rank checksums after timing.
+
+--impl reference: the CPU oracle (oracle/, plain sequential C) timed on the
+host on a bounded sample of the same workload, same metric and unit.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+# ---- launch configurations (shared with the full-size parity tests) ----------
+MS_N = 1 << 24
+MS_CUTOFF = 128
+MS_CFG = dict(grid_size=0, block_size=128, max_tasks_per_worker=1024)
+FIB_N = 40
+FIB_CFG = dict(grid_size=0, block_size=128, max_tasks_per_worker=4096)
+SPMV_ROWS = 1 << 22
+SPMV_NNZ_CUT = 8192
+SPMV_FANOUT = 16
+SPMV_CFG = dict(grid_size=148 * 4, block_size=256, max_tasks_per_worker=1024)
+BFS_SCALE = 22
+BFS_CFG = dict(grid_size=148 * 4, block_size=256, max_tasks_per_worker=1 << 19)
+
+L2_FLUSH_BYTES = 256 << 20
+METRIC = "Mkeys/s (mergesort 2^24 int32, cutoff 128), device-timed"
+UNIT = "Mkeys/s"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+def profile_traffic(key):
+    """dram bytes per launch from the committed ncu --set full summary, if any."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f).get(key)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------------------- ours
+
+def _dist():
+    import torch.distributed as dist
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1 and not dist.is_initialized():
+        dist.init_process_group("nccl")
+    return ws, rank, local
+
+
+def _max_over_ranks(x, ws):
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def bench_mergesort(args, ws, rank, dev):
+    import torch
+
+    import synth
+    import paper_2604_05982_b200 as g
+
+    n = MS_N
+    pristine = synth.keys_int32(n, seed=42 + rank, device=dev)
+    keys = torch.empty_like(pristine)
+    scratch = torch.empty_like(pristine)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
+    rt = g.Runtime(g.GTAP_WORKER_THREAD, dev.index, **MS_CFG)
+    table = g.Table.mergesort(keys, scratch, MS_CUTOFF)
+    stream = torch.cuda.current_stream()
+
+    def step(timed_events=None):
+        keys.copy_(pristine)
+        flush.fill_(1)
+        rt.reset(stream)
+        rt.spawn_root(table, (0, n))
+        if timed_events:
+            timed_events[0].record(stream)
+        rt.run(stream)
+        if timed_events:
+            timed_events[1].record(stream)
+        return rt.sync()
+
+    for _ in range(args.warmup):
+        step()
+    _barrier(ws)
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    stats = []
+    with ClockSampler(dev.index) as clk:
+        t0 = time.perf_counter()
+        for i in range(args.steps):
+            stats.append(step(evs[i]))
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+    _barrier(ws)
+    ev_ms = [a.elapsed_time(b) for a, b in evs]           # torch events around gtap_run (incl. root/ctl H2D)
+    kern_ms = [s.device_ms for s in stats]                 # runtime events around the persistent kernel only
+    ms = statistics.mean(kern_ms)
+    ms_max = _max_over_ranks(ms, ws)
+    # correctness guard: sorted + checksum (the parity tests compare with the oracle bit for bit)
+    ok = bool(torch.all(keys[1:] >= keys[:-1]).item()) and \
+        int(keys.to(torch.int64).sum().item()) == int(pristine.to(torch.int64).sum().item())
+    # e2e through the public API with host buffers: H2D + sort + D2H every step
+    host_in = pristine.cpu().pin_memory()
+    host_out = torch.empty_like(host_in).pin_memory()
+    e2e_ms = []
+    for i in range(max(2, min(args.steps, 5))):
+        flush.fill_(1)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        keys.copy_(host_in, non_blocking=True)
+        rt.reset(stream)
+        g.mergesort_(keys, scratch, MS_CUTOFF, rt=rt, stream=stream)
+        host_out.copy_(keys, non_blocking=True)
+        b.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms.append(a.elapsed_time(b))
+    e2e_ms_max = _max_over_ranks(statistics.mean(e2e_ms), ws)
+    st = stats[-1]
+    algo_bytes = 8.0 * n * (1 + _ms_levels(n, MS_CUTOFF))  # read+write per key per pass
+    pk, src = peaks()
+    achieved = algo_bytes / (ms * 1e-3) / 1e9
+    span_steps = 2 * n  # sequential merge steps on the critical path (top merge n + next n/2 + ...)
+    res = dict(
+        value=ws * n / (ms_max * 1e-3) / 1e6, ms_per_step=ms_max, wall_ms_per_step=wall * 1e3 / args.steps,
+        event_ms_per_step=statistics.mean(ev_ms),
+        e2e=dict(value=ws * n / (e2e_ms_max * 1e-3) / 1e6, unit=UNIT, h2d_bytes_per_step=4 * n,
+                 d2h_bytes_per_step=4 * n),
+        roofline=dict(bound="hbm", achieved=achieved, peak=pk["hbm_gbs"], unit="GB/s",
+                      frac=achieved / pk["hbm_gbs"], traffic=profile_traffic("mergesort"),
+                      peak_source=src, algorithmic_bytes_per_launch=algo_bytes,
+                      note="span-bound by design: the top merge is one thread (P:593); "
+                           f"critical path ~{span_steps} sequential merge steps, "
+                           f"{ms * 1e6 / span_steps:.2f} ns per step"),
+        stats=dict(tasks=st.tasks, invocations=st.invocations, steals_ok=st.steals_ok, workers=st.workers,
+                   grid=st.grid_size, block=st.block_size),
+        correct=ok, clocks=clk.summary(), gpu_launches=args.steps,
+    )
+    rt.close()
+    table.close()
+    return res
+
+
+def _ms_levels(n, c):
+    lv = 0
+    while n > c:
+        n = (n + 1) // 2
+        lv += 1
+    return lv
+
+
+def bench_fib(dev, reps=3):
+    import torch
+
+    import paper_2604_05982_b200 as g
+    rt = g.Runtime(g.GTAP_WORKER_THREAD, dev.index, **FIB_CFG)
+    ms = []
+    st = None
+    for i in range(reps + 1):
+        v, st = g.fib(FIB_N, rt=rt)
+        assert v == 102334155
+        if i:
+            ms.append(st.device_ms)
+    rt.close()
+    t = statistics.median(ms)
+    tasks = st.tasks
+    return dict(workload="fib(40) no cutoff, thread-level (configs[2])", metric="tasks/s", value=tasks / (t * 1e-3),
+                ms=t, tasks=tasks, invocations=st.invocations, workers=st.workers, steals_ok=st.steals_ok,
+                join_atomics=tasks - 1)
+
+
+def bench_atomics(dev):
+    import torch
+
+    import paper_2604_05982_b200 as g
+    buf = torch.empty(1 << 26, dtype=torch.int32, device=dev)  # 256 MiB: words spread over L2 + HBM
+    small = torch.empty(1 << 22, dtype=torch.int32, device=dev)  # 16 MiB: L2-resident
+    out = {}
+    grid, block, ops = 148 * 8, 256, 64
+    for name, kind in (("atom_add_relaxed", 0), ("red_add", 1), ("atom_cas", 2), ("atom_min", 3),
+                       ("same_address_add", 4), ("atom_add_acq_rel", 5)):
+        b = small
+        g.ubench_atomics(b, kind, grid, block, ops)
+        ms = min(g.ubench_atomics(b, kind, grid, block, ops if kind != 4 else 4) for _ in range(3))
+        nops = grid * block * (ops if kind != 4 else 4)
+        out[name] = nops / (ms * 1e-3)
+    return out
+
+
+def bench_spmv(dev, reps=5):
+    import torch
+
+    import synth
+    import paper_2604_05982_b200 as g
+    rp, col, val, x = synth.powerlaw_csr(SPMV_ROWS, seed=7, device=dev)
+    y = torch.empty(SPMV_ROWS, dtype=torch.float32, device=dev)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
+    rt = g.Runtime(g.GTAP_WORKER_BLOCK, dev.index, **SPMV_CFG)
+    ms = []
+    st = None
+    for i in range(reps + 1):
+        flush.fill_(1)
+        rt.reset()
+        y, st = g.spmv(rp, col, val, x, y, SPMV_NNZ_CUT, SPMV_FANOUT, rt=rt)
+        if i:
+            ms.append(st.device_ms)
+    rt.close()
+    t = statistics.median(ms)
+    nnz = int(rp[-1].item())
+    algo = 8.0 * nnz + 12.0 * SPMV_ROWS  # col+val per nnz; row_ptr + y + x once per row
+    pk, _ = peaks()
+    return dict(workload="SpMV power-law 2^22 rows (configs[3]), block-level", metric="GB/s",
+                value=algo / (t * 1e-3) / 1e9, gflops=2.0 * nnz / (t * 1e-3) / 1e9, ms=t, nnz=nnz,
+                tasks=st.tasks, frac_hbm=algo / (t * 1e-3) / 1e9 / pk["hbm_gbs"], traffic=profile_traffic("spmv"))
+
+
+def bench_bfs(dev, nsrc=4):
+    import torch
+
+    import synth
+    import paper_2604_05982_b200 as g
+    rp, col = synth.rmat_csr(BFS_SCALE, 16, seed=3, device=dev)
+    depth = torch.empty(rp.numel() - 1, dtype=torch.int32, device=dev)
+    rt = g.Runtime(g.GTAP_WORKER_BLOCK, dev.index, **BFS_CFG)
+    srcs = synth.bfs_sources(rp, nsrc + 1, seed=5)
+    res = []
+    for i, s in enumerate(srcs):
+        rt.reset()
+        depth, st = g.bfs(rp, col, s, depth, rt=rt)
+        if i == 0:
+            continue
+        reached = depth != 0x7FFFFFFF
+        deg = (rp[1:] - rp[:-1]).to(torch.int64)
+        edges = int(deg[reached].sum().item()) // 2  # undirected input edges in the component (Graph500)
+        res.append((edges / (st.device_ms * 1e-3), st.device_ms, st.tasks, int(reached.sum().item())))
+    rt.close()
+    teps = statistics.median(r[0] for r in res)
+    return dict(workload="BFS RMAT scale 22 ef 16 (configs[4]), block-level", metric="GTEPS", value=teps / 1e9,
+                ms=statistics.median(r[1] for r in res), tasks=[r[2] for r in res], reached=[r[3] for r in res],
+                sources=len(res))
+
+
+def cpu_baseline(sample_n=1 << 22, budget_s=12.0):
+    """The oracle as it stands (sequential C mergesort), on the host, bounded sample."""
+    import oracle
+    import synth
+    keys = synth.keys_int32(sample_n, seed=11).numpy()
+    oracle.mergesort(keys[:1024], MS_CUTOFF)
+    t_tot, reps = 0.0, 0
+    while t_tot < budget_s and reps < 50:
+        t0 = time.perf_counter()
+        oracle.mergesort(keys, MS_CUTOFF)
+        t_tot += time.perf_counter() - t0
+        reps += 1
+    return dict(value=sample_n * reps / t_tot / 1e6, unit=UNIT, cores=1, kind="oracle",
+                sample=f"{reps} x oracle mergesort of 2^{sample_n.bit_length() - 1} seeded int32 keys, cutoff 128")
+
+
+def run_ours(args):
+    import torch
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    res = bench_mergesort(args, ws, rank, dev)
+    secondary = []
+    if not args.no_secondary:
+        try:
+            atoms = bench_atomics(dev)
+            fibr = bench_fib(dev)
+            peak_atom = atoms["atom_add_acq_rel"]
+            fibr["roofline"] = dict(bound="l2_atomic", achieved=fibr["join_atomics"] / (fibr["ms"] * 1e-3),
+                                    peak=peak_atom, unit="atomics/s",
+                                    frac=fibr["join_atomics"] / (fibr["ms"] * 1e-3) / peak_atom,
+                                    peak_source="measured live: gtap_ubench_atomics kind 5 (atom.acq_rel.add, "
+                                                "distinct L2-resident sectors)")
+            secondary.append(fibr)
+            secondary.append(dict(workload="L2 atomic probes", metric="ops/s", value=atoms))
+        except Exception as e:  # secondary results must not kill the main line
+            secondary.append(dict(workload="fib40/atomics", error=repr(e)))
+        for fn in (bench_spmv, bench_bfs):
+            try:
+                secondary.append(fn(dev))
+            except Exception as e:
+                secondary.append(dict(workload=fn.__name__, error=repr(e)))
+    # the only collective: gather per-rank checksums after timing
+    if ws > 1:
+        import torch.distributed as dist
+        t = torch.tensor([1.0 if res["correct"] else 0.0], device=dev)
+        allv = [torch.zeros_like(t) for _ in range(ws)]
+        dist.all_gather(allv, t)
+        res["correct"] = all(bool(v.item()) for v in allv)
+    if rank == 0:
+        pk, src = peaks()
+        line = {
+            "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": res["ms_per_step"], "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "config": {"workload": "mergesort 2^24 random int32 keys, thread-level fork-join, cutoff 128 "
+                                   "(BASELINE configs[1])",
+                       "keys_per_gpu": MS_N, "cutoff": MS_CUTOFF, "launch": MS_CFG,
+                       "grid": res["stats"]["grid"], "block": res["stats"]["block"],
+                       "workers": res["stats"]["workers"], "l2": "flushed between steps (256 MiB write)",
+                       "parallelism": f"replicas x{ws} (independent roots per GPU)",
+                       "timing": "persistent-kernel CUDA events (PAPER P:323); input restore, L2 flush and "
+                                 "gtap_reset untimed between steps"},
+            "e2e": res["e2e"], "roofline": res["roofline"], "gpu_launches": res["gpu_launches"],
+            "clocks": res["clocks"], "correct": res["correct"], "stats": res["stats"],
+            "wall_ms_per_step": res["wall_ms_per_step"], "event_ms_per_step": res["event_ms_per_step"],
+            "secondary": secondary,
+        }
+        if ws == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline()
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def run_reference(args):
+    """The CPU oracle as it stands, timed on the host (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    import oracle
+    import synth
+    sample_n = 1 << 21
+    keys = synth.keys_int32(sample_n, seed=11).numpy()
+    for _ in range(args.warmup):
+        oracle.mergesort(keys[: 1 << 16], MS_CUTOFF)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.mergesort(keys, MS_CUTOFF)
+        times.append(time.perf_counter() - t0)
+    t = statistics.mean(times)
+    v = sample_n / t / 1e6
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": {"workload": "mergesort 2^24 random int32 keys, cutoff 128 (BASELINE configs[1]); "
+                               "each step sorts a bounded 2^21-key sample"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": f"2^21 seeded int32 keys per step, {args.steps} steps"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

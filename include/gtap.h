@@ -1,0 +1,215 @@
+/*
+ * gtap.h -- C ABI of the B200-native GTaP hot path: a device-resident,
+ * persistent-kernel fork-join scheduler (§4) behind plain
+ * pointers and sizes. No torch types cross this boundary; the Python binding
+ * (paper_2604_05982_b200/gtap.py) only marshals arguments.
+ *
+ * Paper mapping (P:n = line n of reference/PAPER.md):
+ *   gtap_initialize() pre-allocates task storage (§5.1.2)
+ *                                             -> gtap_workspace_bytes + gtap_init
+ *   #pragma gtap entry: enqueue root + start
+ *                                             -> gtap_spawn_root + gtap_run
+ *   exec_kernel<<<GRID,BLOCK>>> + cudaDeviceSynchronize
+ *                                             -> gtap_run + gtap_sync
+ *   cudaMemcpyFromSymbol(&h_result, d_result) -> gtap_root_result
+ *   gtap_finalize()                  -> gtap_finalize
+ *   compile-time capacity macros (Table "Preprocessor macros")
+ *                                             -> gtap_config fields
+ *   #pragma gtap function task bodies -> per-benchmark task
+ *                                                 tables (gtap_table_*)
+ *
+ * Conventions (every call):
+ *   - returns gtap_status; nothing aborts, throws or prints;
+ *   - device pointers are plain CUDA device addresses on the runtime's device
+ *     (e.g. torch.Tensor.data_ptr()); they are caller-owned and must stay
+ *     alive until gtap_sync returns for the run that uses them;
+ *   - a cudaStream_t is passed as void* (NULL = legacy default stream);
+ *   - one runtime per device per process thread; a runtime runs one table at
+ *     a time; all roots of a run use that run's table.
+ */
+#ifndef GTAP_H
+#define GTAP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GTAP_ABI_VERSION 1u
+
+typedef enum {
+    GTAP_OK = 0,
+    GTAP_E_INVAL = 1,          /* bad argument / configuration */
+    GTAP_E_CUDA = 2,           /* a CUDA runtime call failed */
+    GTAP_E_NOMEM = 3,          /* device or host allocation failed */
+    GTAP_E_BUSY = 4,           /* a run is in flight (call gtap_sync first) */
+    GTAP_E_POOL_EXHAUSTED = 5, /* a worker's task-record pool ran out */
+    GTAP_E_QUEUE_OVERFLOW = 6, /* a deque ring overflowed (fixed capacity) */
+    GTAP_E_CHILD_LIMIT = 7,    /* > max_child_tasks spawns in one invocation */
+    GTAP_E_TIMEOUT = 8,        /* liveness watchdog expired (config.watchdog_ns) */
+    GTAP_E_BAD_STATE = 9,      /* unknown (task function, state) dispatched (P:1188 default:) */
+    GTAP_E_NO_DEVICE = 10,     /* no CUDA device / not sm_100 */
+    GTAP_E_UNSUPPORTED = 11    /* table/config combination not built */
+} gtap_status;
+
+typedef enum {
+    GTAP_WORKER_THREAD = 0,    /* thread-executed: one CUDA thread runs one task */
+    GTAP_WORKER_BLOCK = 1      /* block-cooperative: one block runs one task */
+} gtap_worker_kind;
+
+/* Runtime configuration: the paper's compile-time macros as run-time fields.
+ * Zero means "default" where stated. */
+typedef struct {
+    uint32_t struct_size;          /* = sizeof(gtap_config); ABI guard */
+    int32_t  device;               /* CUDA ordinal of this process's GPU */
+    uint32_t worker_kind;          /* gtap_worker_kind */
+    uint32_t grid_size;            /* GTAP_GRID_SIZE; 0 = all co-resident blocks */
+    uint32_t block_size;           /* GTAP_BLOCK_SIZE; multiple of 32; 0 = 128 */
+    uint32_t max_tasks_per_worker; /* GTAP_MAX_TASKS_PER_WARP / _PER_BLOCK;
+                                      records per worker pool, power of two; 0 = 4096 */
+    uint32_t queue_capacity;       /* ring slots per deque, power of two; 0 = max_tasks_per_worker */
+    uint32_t max_child_tasks;      /* GTAP_MAX_CHILD_TASKS; 0 = table's own bound */
+    uint32_t num_queues;           /* GTAP_NUM_QUEUES (EPAQ); 1 in this build */
+    uint32_t max_task_data_size;   /* GTAP_MAX_TASK_DATA_SIZE bytes; 0 = 16 */
+    uint32_t assume_no_taskwait;   /* GTAP_ASSUME_NO_TASKWAIT; informative:
+                                      tables that never join set it themselves */
+    uint32_t steal_attempts;       /* victims probed per idle cycle; 0 = 4 */
+    uint32_t steal_max;            /* max tasks per steal; 0 = 32 (warp) / 1 (block) */
+    uint32_t max_roots;            /* forest capacity (roots per run); 0 = 65536 */
+    uint64_t seed;                 /* victim-selection PRNG seed */
+    uint64_t watchdog_ns;          /* 0 = off; else a run longer than this fails with GTAP_E_TIMEOUT */
+} gtap_config;
+
+typedef struct gtap_runtime gtap_runtime;
+typedef struct gtap_task_table gtap_task_table;
+
+/* Counters of one run, summed over workers on the device at kernel exit. */
+typedef struct {
+    uint64_t tasks;            /* task records created (roots included) */
+    uint64_t invocations;      /* task-function invocations (one per state executed) */
+    uint64_t pops;             /* tasks taken from the worker's own deque */
+    uint64_t kept;             /* tasks run from the keep-for-next-cycle set */
+    uint64_t steals_ok;        /* successful steal operations */
+    uint64_t steals_failed;    /* steal attempts that found nothing or lost the race */
+    uint64_t stolen_tasks;     /* tasks moved by steals */
+    uint64_t pushes;           /* tasks written to deques */
+    uint64_t cycles;           /* scheduler loop iterations that executed >= 1 task */
+    uint64_t idle_cycles;      /* scheduler loop iterations without a task */
+    uint64_t remote_frees;     /* records freed by a worker other than their home */
+    uint64_t max_pool_used;    /* max records ever drawn from one worker's bump region */
+    uint32_t error_word;       /* gtap_status set on the device (0 = none) */
+    uint32_t workers;          /* warps (thread-level) or blocks (block-level) */
+    float    device_ms;        /* CUDA-event time of the persistent kernel */
+    uint32_t grid_size;        /* launched grid */
+    uint32_t block_size;       /* launched block */
+    uint32_t reserved[2];
+} gtap_stats;
+
+/* ---- lifecycle ---------------------------------------------------------- */
+
+/* Version of this ABI (GTAP_ABI_VERSION). */
+uint32_t gtap_abi_version(void);
+
+/* Human-readable name of a status code (static storage, never NULL). */
+const char *gtap_status_str(gtap_status s);
+
+/* Fill *cfg with defaults for `kind` on `device` (struct_size set). */
+gtap_status gtap_config_default(gtap_config *cfg, int32_t device, uint32_t kind);
+
+/* Device bytes gtap_init needs for *cfg (0 on invalid cfg). Layout: task
+ * records (32 B each, 16-B aligned), deque rings, per-deque metadata lines,
+ * per-worker free rings, control block. */
+size_t gtap_workspace_bytes(const gtap_config *cfg);
+
+/* Create a runtime ("pre-allocates the memory regions required for
+ * task management on the host side"). d_workspace: caller-owned device buffer
+ * of >= gtap_workspace_bytes(cfg) bytes, 256-B aligned, or NULL to let the
+ * runtime cudaMalloc (and free) it. On success *out is a new runtime. */
+gtap_status gtap_init(const gtap_config *cfg, void *d_workspace, size_t bytes, gtap_runtime **out);
+
+/* Stage a root task ("entry enqueues the initial (root) task"). The
+ * args (nbytes <= 16) are copied now (firstprivate). Several calls
+ * before one gtap_run make a forest; roots are spread round-robin over the
+ * workers. *root_idx (may be NULL) indexes gtap_root_result. All roots of a
+ * run must use the same table. */
+gtap_status gtap_spawn_root(gtap_runtime *rt, const gtap_task_table *table, uint32_t fn,
+                            const void *args, uint32_t nbytes, uint32_t *root_idx);
+
+/* Re-arm the workspace for a new run (zero queues, pools, counters; drop
+ * staged roots). Asynchronous on `stream`. */
+gtap_status gtap_reset(gtap_runtime *rt, void *stream);
+
+/* Launch the persistent kernel for the staged roots on `stream` (async).
+ * Implies gtap_reset unless the runtime was reset since the last run.
+ * Returns GTAP_E_BUSY if a run is in flight, GTAP_E_INVAL if no root is
+ * staged or the grid cannot be co-resident. */
+gtap_status gtap_run(gtap_runtime *rt, void *stream);
+
+/* Block until the run finishes; decode the device error word; fill *out
+ * (may be NULL). Returns the device error (GTAP_E_POOL_EXHAUSTED, ...) if any. */
+gtap_status gtap_sync(gtap_runtime *rt, gtap_stats *out);
+
+/* Copy root result `root_idx` (int64 on the device) into *out
+ * (nbytes <= 8, little-endian truncation). Valid after gtap_sync. */
+gtap_status gtap_root_result(gtap_runtime *rt, uint32_t root_idx, void *out, uint32_t nbytes);
+
+/* Release everything gtap_init allocated. rt may be NULL. */
+gtap_status gtap_finalize(gtap_runtime *rt);
+
+/* Effective launch geometry of `table` on this runtime (after defaults and
+ * the occupancy clamp): workers, grid, block. */
+gtap_status gtap_geometry(gtap_runtime *rt, const gtap_task_table *table,
+                          uint32_t *workers, uint32_t *grid, uint32_t *block);
+
+/* ---- task tables (the "#pragma gtap function" bodies, hand-transformed) -- */
+
+/* Free a table returned by a gtap_table_* constructor (NULL ok). */
+void gtap_table_destroy(const gtap_task_table *t);
+
+/* fib (P:1023-1033 + transformed P:1160-1190), thread-level, no cutoff.
+ * fn 0, root args {int32 n}, 0 <= n <= 46; result int64 fib(n). */
+const gtap_task_table *gtap_table_fib(void);
+
+/* mergesort with cutoff (state machine P:59-74), thread-level.
+ * keys: int32[n] device buffer sorted in place; scratch: int32[n] device
+ * buffer (ping-pong target); cutoff in [1, 256]. fn 0, root args
+ * {uint32 l, uint32 r} (normally {0, n}); result 0. */
+const gtap_task_table *gtap_table_mergesort(int32_t *keys, int32_t *scratch, uint64_t n,
+                                            int32_t cutoff);
+
+/* SpMV y = A x over CSR (P:42 names SpMV as block-cooperative), block-level,
+ * no taskwait. Task spmv(lo, hi) splits the row range into `fanout` equal
+ * parts while it holds more than nnz_cut non-zeros (and > 1 row); leaves are
+ * computed cooperatively by the block in fp32. fn 0, root args
+ * {uint32 lo, uint32 hi}. y rows outside roots' ranges are untouched. */
+const gtap_task_table *gtap_table_spmv(const int32_t *row_ptr, const int32_t *col,
+                                       const float *val, const float *x, float *y,
+                                       uint32_t nrows, uint32_t nnz_cut, uint32_t fanout);
+
+/* BFS frontier expansion, block-level, no taskwait.
+ * depth: int32[nv], caller sets INT32_MAX everywhere and 0 at the source
+ * before the run (reading R18). fn 0, root args {int32 v}. */
+const gtap_task_table *gtap_table_bfs(const int32_t *row_ptr, const int32_t *col,
+                                      int32_t *depth, uint32_t nv);
+
+/* BFS input preparation (reading R18): depth[v] = INT32_MAX for v != src,
+ * depth[src] = 0, asynchronously on `stream`. */
+gtap_status gtap_bfs_init_depth(int32_t *depth, uint32_t nv, int32_t src, void *stream);
+
+/* ---- microbenchmarks (roofline denominators) ----------- */
+
+/* L2-atomic throughput probe on `stream`, synchronous. kind: 0 atom.add with
+ * return on distinct words (the join decrement), 1 red.add (no return),
+ * 2 atom.cas, 3 atom.min, 4 same-address atom.add. d_buf: device buffer of
+ * >= words*4 bytes (zeroed by the call). ops_per_thread atomics per thread on
+ * grid x block threads. *ms = kernel time. */
+gtap_status gtap_ubench_atomics(void *d_buf, uint64_t words, uint32_t kind, uint32_t grid,
+                                uint32_t block, uint32_t ops_per_thread, void *stream, float *ms);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GTAP_H */

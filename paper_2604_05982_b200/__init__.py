@@ -1,0 +1,117 @@
+"""B200-native GTaP hot path: a persistent-kernel fork-join scheduler (sm_100a).
+
+User-facing calls (each runs the whole path in libgtap.so's CUDA kernels and
+fails loudly when the library or the GPU is missing -- there is no CPU path):
+
+    fib(n)                       -> (F(n), stats)      thread-level
+    mergesort_(keys)             -> stats (in place)   thread-level
+    mergesort_forest_(keys, seg) -> stats              independent roots (forest)
+    spmv(row_ptr, col, val, x)   -> (y, stats)         block-level
+    bfs(row_ptr, col, src)       -> (depth, stats)     block-level
+
+Lower level: gtap.Runtime / gtap.Table mirror include/gtap.h one to one.
+"""
+from __future__ import annotations
+
+from . import gtap
+from .gtap import (GTAP_WORKER_BLOCK, GTAP_WORKER_THREAD, GtapError, Runtime, RunStats, Table,
+                   bfs_init_depth, ubench_atomics)
+
+__all__ = ["gtap", "Runtime", "Table", "RunStats", "GtapError", "fib", "mergesort_", "mergesort_forest_",
+           "spmv", "bfs", "ubench_atomics", "GTAP_WORKER_THREAD", "GTAP_WORKER_BLOCK"]
+
+
+def _runtime(kind, rt, device, cfg):
+    if rt is not None:
+        return rt, False
+    return Runtime(kind, device, **cfg), True
+
+
+def fib(n: int, rt: Runtime | None = None, device: int = 0, stream=None, **cfg):
+    """fib(n) as the paper's no-cutoff task program on thread-level workers."""
+    rt, own = _runtime(GTAP_WORKER_THREAD, rt, device, cfg)
+    table = Table.fib()
+    try:
+        rt.spawn_root(table, (n,))
+        rt.run(stream)
+        st = rt.sync()
+        return rt.root_result(0), st
+    finally:
+        table.close()
+        if own:
+            rt.close()
+
+
+def mergesort_(keys, scratch=None, cutoff: int = 128, rt: Runtime | None = None, stream=None, **cfg):
+    """Sort a CUDA int32 tensor in place with the cutoff mergesort task program."""
+    import torch
+    if scratch is None:
+        scratch = torch.empty_like(keys)
+    rt, own = _runtime(GTAP_WORKER_THREAD, rt, keys.device.index or 0, cfg)
+    table = Table.mergesort(keys, scratch, cutoff)
+    try:
+        rt.spawn_root(table, (0, keys.numel()))
+        rt.run(stream)
+        return rt.sync()
+    finally:
+        table.close()
+        if own:
+            rt.close()
+
+
+def mergesort_forest_(keys, segments, scratch=None, cutoff: int = 128, rt: Runtime | None = None, stream=None,
+                      **cfg):
+    """Sort independent segments [(l, r), ...] of one CUDA int32 tensor: one root per segment."""
+    import torch
+    if scratch is None:
+        scratch = torch.empty_like(keys)
+    cfg.setdefault("max_roots", max(len(segments), 1))
+    rt, own = _runtime(GTAP_WORKER_THREAD, rt, keys.device.index or 0, cfg)
+    table = Table.mergesort(keys, scratch, cutoff)
+    try:
+        for l, r in segments:
+            rt.spawn_root(table, (l, r))
+        rt.run(stream)
+        return rt.sync()
+    finally:
+        table.close()
+        if own:
+            rt.close()
+
+
+def spmv(row_ptr, col, val, x, y=None, nnz_cut: int = 8192, fanout: int = 16, rows=None,
+         rt: Runtime | None = None, stream=None, **cfg):
+    """y = A x for a CSR matrix with block-cooperative task leaves (rows=(lo, hi) restricts the root)."""
+    import torch
+    if y is None:
+        y = torch.empty(row_ptr.numel() - 1, dtype=torch.float32, device=row_ptr.device)
+    rt, own = _runtime(GTAP_WORKER_BLOCK, rt, row_ptr.device.index or 0, cfg)
+    table = Table.spmv(row_ptr, col, val, x, y, nnz_cut, fanout)
+    lo, hi = rows if rows is not None else (0, row_ptr.numel() - 1)
+    try:
+        rt.spawn_root(table, (lo, hi))
+        rt.run(stream)
+        return y, rt.sync()
+    finally:
+        table.close()
+        if own:
+            rt.close()
+
+
+def bfs(row_ptr, col, src: int, depth=None, rt: Runtime | None = None, stream=None, **cfg):
+    """BFS levels from src (INT32_MAX = unreached) by the paper's frontier-expansion tasks."""
+    import torch
+    nv = row_ptr.numel() - 1
+    if depth is None:
+        depth = torch.empty(nv, dtype=torch.int32, device=row_ptr.device)
+    rt, own = _runtime(GTAP_WORKER_BLOCK, rt, row_ptr.device.index or 0, cfg)
+    table = Table.bfs(row_ptr, col, depth)
+    try:
+        bfs_init_depth(depth, src, stream)
+        rt.spawn_root(table, (src,))
+        rt.run(stream)
+        return depth, rt.sync()
+    finally:
+        table.close()
+        if own:
+            rt.close()

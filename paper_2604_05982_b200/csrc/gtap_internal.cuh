@@ -1,0 +1,302 @@
+// gtap_internal.cuh -- workspace layout and sm_100a primitives shared by the
+// persistent schedulers (sched_thread.cuh, sched_block.cuh) and the host
+// runtime (runtime.cu). Product code: never includes anything from oracle/.
+//
+// Memory-consistency contract (§4.5: per-SM L1 is not
+// coherent; use L1-bypassing accesses + fences for shared metadata):
+//   * every read of shared mutable scheduler state (task records, deque ring
+//     entries, deque metadata, free rings, control words) is a .relaxed.gpu
+//     "strong" load (SASS LDG.E.STRONG.GPU: served by L2, never a stale L1
+//     line) -- the sm_100a spelling of the paper's ld.global.cg;
+//   * publication edges use release (MEMBAR.ALL.GPU + op): deque publication
+//     (red.release on the packed head|split word) and the join decrement
+//     (atom.acq_rel);
+//   * every edge that hands a runnable task to another warp/SM ends in an
+//     acquire on the receiving SM (steal CAS .acquire, join decrement
+//     .acq_rel), which also invalidates that SM's L1 (CCTL.IVALL), so task
+//     bodies may use ordinary cached loads for data their ancestors wrote.
+#pragma once
+#include <cstdint>
+
+#ifndef GTAP_HOST_ONLY
+#include <cuda_runtime.h>
+#endif
+
+namespace gtap {
+
+constexpr uint32_t kNone = 0xFFFFFFFFu;
+constexpr uint32_t kRootFlag = 0x80000000u;
+constexpr int kDataWords = 4;  // 16-B payload per record (GTAP_MAX_TASK_DATA_SIZE default)
+
+// Task record ("(i) a payload ... and (ii) metadata ... the task
+// function, parent/child IDs, and a resumption state"). 32 B = one L2 sector;
+// two 16-B vector accesses. Child results land in the parent's data[2 + ordinal]
+// (copy-at-finish, R8), so a finished child's record is freed at once.
+struct __align__(32) TaskRec {
+    uint32_t meta;     // fn:8 | state:8 | ordinal:8 | queue:8
+    int32_t pending;   // outstanding children of the current join epoch
+    uint32_t parent;   // parent record id, kNone for roots / no-taskwait tasks
+    uint32_t aux;      // kRootFlag | root index for roots, else 0
+    uint32_t d[kDataWords];
+};
+static_assert(sizeof(TaskRec) == 32, "record must be one 32-B sector");
+
+__host__ __device__ inline uint32_t make_meta(uint32_t fn, uint32_t state, uint32_t ord, uint32_t q) {
+    return (fn & 0xFF) | ((state & 0xFF) << 8) | ((ord & 0xFF) << 16) | ((q & 0xFF) << 24);
+}
+__host__ __device__ inline uint32_t meta_fn(uint32_t m) { return m & 0xFF; }
+__host__ __device__ inline uint32_t meta_state(uint32_t m) { return (m >> 8) & 0xFF; }
+__host__ __device__ inline uint32_t meta_ord(uint32_t m) { return (m >> 16) & 0xFF; }
+
+// Per-deque shared metadata, one 64-B line each (no false sharing between
+// victims). S packs head (steal end, low 32 bits) and split (high 32 bits):
+// [head, split) is public (stealable), [split, tail) is the owner's private
+// part (tail lives in the owner's registers, "tail is kept in
+// shared memory because only the owner warp updates it").
+struct __align__(64) DequeMeta {
+    unsigned long long S;   // head | split << 32   (CAS by thieves / owner reclaim, red.add by owner publish)
+    uint32_t steal_done;    // tasks whose ring slots thieves have finished reading
+    uint32_t lock;          // serialises thieves of this deque
+    uint32_t pad[12];
+};
+static_assert(sizeof(DequeMeta) == 64, "");
+
+// Per-worker free-record ring (MPSC: any worker frees, the home worker
+// allocates). Entries hold id+1 (0 = not yet written).
+struct __align__(64) FreeMeta {
+    uint32_t tail;          // producers atomicAdd
+    uint32_t pad[15];
+};
+
+enum StatIdx : int {
+    ST_TASKS = 0, ST_INVOC, ST_POPS, ST_KEPT, ST_STEALS_OK, ST_STEALS_FAILED, ST_STOLEN,
+    ST_PUSHES, ST_CYCLES, ST_IDLE, ST_REMOTE_FREES, ST_MAX_POOL, ST_COUNT = 16
+};
+
+// Control block: each hot word on its own 128-B line.
+struct __align__(128) Ctl {
+    uint32_t done;            // termination flag (set once)
+    uint32_t pad0[31];
+    uint32_t error;           // sticky gtap_status
+    uint32_t pad1[31];
+    long long outstanding;    // no-taskwait termination counter (SPEC S:321 reading)
+    uint32_t pad2[30];
+    uint32_t roots_left;      // taskwait-closed termination: roots not yet finished
+    uint32_t pad3[31];
+    unsigned long long stats[ST_COUNT];
+    uint32_t pad4[32];
+};
+
+struct RootSpec {
+    uint32_t fn;
+    uint32_t d[kDataWords];
+};
+
+// Kernel parameters (by value): geometry + device pointers into one workspace.
+struct KParams {
+    uint32_t W;              // workers (warps or blocks)
+    uint32_t logM;           // records per worker = 1 << logM
+    uint32_t qmask;          // ring capacity - 1 (power of two)
+    uint32_t steal_rounds;   // probe rounds per idle cycle
+    uint32_t steal_max;      // max tasks per steal
+    uint32_t nroots;
+    uint32_t max_child;      // GTAP_MAX_CHILD_TASKS (runtime check)
+    uint32_t pad;
+    unsigned long long seed;
+    unsigned long long watchdog_ns;
+    TaskRec* rec;            // W << logM records
+    uint32_t* ring;          // W * (qmask+1)
+    DequeMeta* dq;           // W
+    uint32_t* fring;         // W << logM
+    FreeMeta* fm;            // W
+    Ctl* ctl;
+    const RootSpec* roots;   // nroots
+    long long* root_results; // nroots
+};
+
+// Host-side layout of the workspace (offsets in bytes).
+struct Layout {
+    size_t rec, ring, dq, fring, fm, ctl, roots, results, total;
+    uint32_t W, M, Q, max_roots;
+};
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+inline Layout make_layout(uint32_t W, uint32_t M, uint32_t Q, uint32_t max_roots) {
+    Layout L{};
+    L.W = W; L.M = M; L.Q = Q; L.max_roots = max_roots;
+    size_t o = 0;
+    L.ctl = o;     o = align_up(o + sizeof(Ctl), 256);
+    L.dq = o;      o = align_up(o + sizeof(DequeMeta) * (size_t)W, 256);
+    L.fm = o;      o = align_up(o + sizeof(FreeMeta) * (size_t)W, 256);
+    L.roots = o;   o = align_up(o + sizeof(RootSpec) * (size_t)max_roots, 256);
+    L.results = o; o = align_up(o + sizeof(long long) * (size_t)max_roots, 256);
+    L.fring = o;   o = align_up(o + sizeof(uint32_t) * (size_t)W * M, 256);
+    L.ring = o;    o = align_up(o + sizeof(uint32_t) * (size_t)W * Q, 256);
+    L.rec = o;     o = align_up(o + sizeof(TaskRec) * (size_t)W * M, 256);
+    L.total = o;
+    return L;
+}
+
+// Bytes that gtap_reset must zero: control block, deque metadata, free-ring
+// metadata, and the free rings themselves (entries 0 = empty).
+inline size_t reset_span_front(const Layout& L) { return L.roots; }
+
+}  // namespace gtap
+
+#ifndef GTAP_HOST_ONLY
+namespace gtap {
+namespace dev {
+
+// ---- strong (L1-bypassing, L2-coherent) accesses ---------------------------
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ int32_t ld_relaxed(const int32_t* p) {
+    int32_t v;
+    asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ long long ld_relaxed(const long long* p) {
+    long long v;
+    asm volatile("ld.relaxed.gpu.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint4 ld_relaxed_v4(const void* p) {
+    uint4 v;
+    asm volatile("ld.relaxed.gpu.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed(uint32_t* p, uint32_t v) {
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed(int32_t* p, int32_t v) {
+    asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// weak vector store (published later by a release)
+__device__ __forceinline__ void st_v4(void* p, uint4 v) {
+    asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ void st_v2(void* p, uint32_t a, uint32_t b) {
+    asm volatile("st.global.v2.u32 [%0], {%1,%2};" ::"l"(p), "r"(a), "r"(b) : "memory");
+}
+
+// ---- atomics ----------------------------------------------------------------
+__device__ __forceinline__ int32_t atom_add_acq_rel(int32_t* p, int32_t v) {
+    int32_t o;
+    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(o) : "l"(p), "r"(v) : "memory");
+    return o;
+}
+__device__ __forceinline__ uint32_t atom_add_acq_rel(uint32_t* p, uint32_t v) {
+    uint32_t o;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(o) : "l"(p), "r"(v) : "memory");
+    return o;
+}
+__device__ __forceinline__ long long atom_add_acq_rel(long long* p, long long v) {
+    long long o;
+    asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], %2;" : "=l"(o) : "l"(p), "l"(v) : "memory");
+    return o;
+}
+__device__ __forceinline__ uint32_t atom_add_relaxed(uint32_t* p, uint32_t v) {
+    uint32_t o;
+    asm volatile("atom.relaxed.gpu.global.add.u32 %0, [%1], %2;" : "=r"(o) : "l"(p), "r"(v) : "memory");
+    return o;
+}
+__device__ __forceinline__ void red_add_release(unsigned long long* p, unsigned long long v) {
+    asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void red_add_release(uint32_t* p, uint32_t v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_add_relaxed(unsigned long long* p, unsigned long long v) {
+    asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long atom_cas_acquire(unsigned long long* p, unsigned long long cmp,
+                                                              unsigned long long val) {
+    unsigned long long o;
+    asm volatile("atom.acquire.gpu.global.cas.b64 %0, [%1], %2, %3;" : "=l"(o) : "l"(p), "l"(cmp), "l"(val)
+                 : "memory");
+    return o;
+}
+__device__ __forceinline__ unsigned long long atom_cas_relaxed(unsigned long long* p, unsigned long long cmp,
+                                                              unsigned long long val) {
+    unsigned long long o;
+    asm volatile("atom.relaxed.gpu.global.cas.b64 %0, [%1], %2, %3;" : "=l"(o) : "l"(p), "l"(cmp), "l"(val)
+                 : "memory");
+    return o;
+}
+__device__ __forceinline__ uint32_t atom_cas_relaxed(uint32_t* p, uint32_t cmp, uint32_t val) {
+    uint32_t o;
+    asm volatile("atom.relaxed.gpu.global.cas.b32 %0, [%1], %2, %3;" : "=r"(o) : "l"(p), "r"(cmp), "r"(val)
+                 : "memory");
+    return o;
+}
+__device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void nanosleep(uint32_t ns) { asm volatile("nanosleep.u32 %0;" ::"r"(ns)); }
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+__device__ __forceinline__ uint32_t xorshift32(uint32_t& s) {
+    s ^= s << 13;
+    s ^= s >> 17;
+    s ^= s << 5;
+    return s;
+}
+
+__device__ __forceinline__ uint32_t hash32(unsigned long long x) {
+    x ^= x >> 33;
+    x *= 0xff51afd7ed558ccdULL;
+    x ^= x >> 33;
+    x *= 0xc4ceb9fe1a85ec53ULL;
+    x ^= x >> 33;
+    return (uint32_t)x | 1u;
+}
+
+// Warp-wide exclusive prefix sum of v (all 32 lanes participate).
+__device__ __forceinline__ uint32_t warp_excl_scan(uint32_t v, uint32_t lane, uint32_t& total) {
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= (uint32_t)o) x += y;
+    }
+    total = __shfl_sync(0xffffffffu, x, 31);
+    return x - v;
+}
+
+// Sticky device error: first writer wins; also raises the termination flag.
+__device__ __forceinline__ void raise_error(Ctl* ctl, uint32_t code) {
+    atom_cas_relaxed(&ctl->error, 0u, code);
+    st_release(&ctl->done, 1u);
+}
+
+}  // namespace dev
+}  // namespace gtap
+#endif

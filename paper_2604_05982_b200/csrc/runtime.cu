@@ -1,0 +1,378 @@
+// runtime.cu -- host side of the C ABI (include/gtap.h).
+//
+// gtap_init bulk-allocates every task-management region on the host before any
+// spawn; gtap_run launches ONE persistent kernel
+// per run with the staged roots; gtap_sync waits, reads the
+// sticky device error word and the device-side counters. Nothing here touches
+// task data: every step of the hot path runs in the kernels of sched_*.cuh.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "gtap.h"
+#include "table_common.cuh"
+
+using gtap::Ctl;
+using gtap::KParams;
+using gtap::Layout;
+using gtap::RootSpec;
+
+struct gtap_runtime {
+    gtap_config cfg;
+    int device;
+    int sm_count;
+    uint32_t wpb;          // workers per block (thread-level: warps per block; block-level: 1)
+    uint32_t W_alloc;      // workers the workspace is sized for
+    uint32_t M, Q, max_roots;
+    Layout L;
+    char* ws;
+    bool owns_ws;
+    std::vector<RootSpec> roots;
+    const gtap_task_table* table;
+    RootSpec* h_roots;     // pinned staging (max_roots)
+    Ctl* h_ctl;            // pinned: control block staging / readback
+    cudaEvent_t ev0, ev1;
+    bool in_flight;
+    bool dirty;            // workspace used since the last reset
+    uint32_t run_grid, run_block, run_W;
+    uint32_t run_nroots;
+    gtap_status last_launch;
+};
+
+namespace {
+
+bool is_pow2(uint32_t x) { return x && !(x & (x - 1)); }
+uint32_t log2u(uint32_t x) { uint32_t l = 0; while ((1u << l) < x) ++l; return l; }
+
+gtap_status cuda_status(cudaError_t e) { return e == cudaSuccess ? GTAP_OK : GTAP_E_CUDA; }
+
+// resolve defaults; returns GTAP_E_INVAL for bad fields
+gtap_status resolve(const gtap_config* in, gtap_config* c, int sm_count) {
+    if (!in || in->struct_size != sizeof(gtap_config)) return GTAP_E_INVAL;
+    *c = *in;
+    if (c->worker_kind > GTAP_WORKER_BLOCK) return GTAP_E_INVAL;
+    if (c->block_size == 0) c->block_size = 128;
+    if (c->block_size % 32 || c->block_size < 32 || c->block_size > 1024) return GTAP_E_INVAL;
+    if (c->max_tasks_per_worker == 0) c->max_tasks_per_worker = 4096;
+    if (!is_pow2(c->max_tasks_per_worker) || c->max_tasks_per_worker < 64 || c->max_tasks_per_worker > (1u << 20))
+        return GTAP_E_INVAL;
+    if (c->queue_capacity == 0) c->queue_capacity = c->max_tasks_per_worker;
+    if (!is_pow2(c->queue_capacity) || c->queue_capacity < 64 || c->queue_capacity > (1u << 24)) return GTAP_E_INVAL;
+    if (c->num_queues == 0) c->num_queues = 1;
+    if (c->num_queues != 1) return GTAP_E_UNSUPPORTED;  // EPAQ: SURVEY §8(f) NEXT #1
+    if (c->max_task_data_size == 0) c->max_task_data_size = 16;
+    if (c->max_task_data_size > 16) return GTAP_E_UNSUPPORTED;
+    if (c->steal_attempts == 0) c->steal_attempts = 4;
+    if (c->steal_max == 0) c->steal_max = (c->worker_kind == GTAP_WORKER_THREAD) ? 32 : 1;
+    if (c->worker_kind == GTAP_WORKER_THREAD && c->steal_max > 32) return GTAP_E_INVAL;
+    if (c->worker_kind == GTAP_WORKER_BLOCK && c->steal_max != 1) return GTAP_E_INVAL;
+    if (c->max_roots == 0) c->max_roots = 65536;
+    const uint32_t wpb = (c->worker_kind == GTAP_WORKER_THREAD) ? c->block_size / 32 : 1;
+    uint64_t W;
+    if (c->grid_size) W = (uint64_t)c->grid_size * wpb;
+    else W = (c->worker_kind == GTAP_WORKER_THREAD) ? (uint64_t)sm_count * 64 : (uint64_t)sm_count * 32;
+    if (W == 0 || W * c->max_tasks_per_worker >= (1ull << 31)) return GTAP_E_INVAL;  // ids are u32, kNone reserved
+    return GTAP_OK;
+}
+
+uint32_t workers_alloc(const gtap_config& c, int sm_count) {
+    const uint32_t wpb = (c.worker_kind == GTAP_WORKER_THREAD) ? c.block_size / 32 : 1;
+    if (c.grid_size) return c.grid_size * wpb;
+    return (c.worker_kind == GTAP_WORKER_THREAD) ? (uint32_t)sm_count * 64 : (uint32_t)sm_count * 32;
+}
+
+int device_sm_count(int dev) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
+    return n;
+}
+
+gtap_status geometry(gtap_runtime* rt, const gtap_task_table* t, uint32_t* W, uint32_t* grid, uint32_t* block) {
+    if (t->kind != rt->cfg.worker_kind) return GTAP_E_INVAL;
+    const uint32_t bs = rt->cfg.block_size;
+    int bps = 0;
+    size_t smem = 0;
+    if (t->occupancy(t, bs, &bps, &smem) != cudaSuccess) return GTAP_E_CUDA;
+    if (bps <= 0) return GTAP_E_INVAL;
+    const uint32_t max_grid = (uint32_t)bps * (uint32_t)rt->sm_count;
+    uint32_t g = rt->cfg.grid_size ? rt->cfg.grid_size : std::min(max_grid, rt->W_alloc / rt->wpb);
+    if (g == 0 || g > max_grid) return GTAP_E_INVAL;  // persistent grid must be co-resident
+    if (g * rt->wpb > rt->W_alloc) return GTAP_E_INVAL;
+    *W = g * rt->wpb;
+    *grid = g;
+    *block = bs;
+    return GTAP_OK;
+}
+
+gtap_status do_reset(gtap_runtime* rt, cudaStream_t s) {
+    cudaSetDevice(rt->device);
+    const Layout& L = rt->L;
+    // control block, deque metadata, free-ring metadata (contiguous at the front)
+    if (cudaMemsetAsync(rt->ws + L.ctl, 0, L.roots - L.ctl, s) != cudaSuccess) return GTAP_E_CUDA;
+    // free rings: entry 0 = empty
+    if (cudaMemsetAsync(rt->ws + L.fring, 0, sizeof(uint32_t) * (size_t)L.W * L.M, s) != cudaSuccess)
+        return GTAP_E_CUDA;
+    rt->dirty = false;
+    return GTAP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+uint32_t gtap_abi_version(void) { return GTAP_ABI_VERSION; }
+
+const char* gtap_status_str(gtap_status s) {
+    switch (s) {
+        case GTAP_OK: return "GTAP_OK";
+        case GTAP_E_INVAL: return "GTAP_E_INVAL";
+        case GTAP_E_CUDA: return "GTAP_E_CUDA";
+        case GTAP_E_NOMEM: return "GTAP_E_NOMEM";
+        case GTAP_E_BUSY: return "GTAP_E_BUSY";
+        case GTAP_E_POOL_EXHAUSTED: return "GTAP_E_POOL_EXHAUSTED";
+        case GTAP_E_QUEUE_OVERFLOW: return "GTAP_E_QUEUE_OVERFLOW";
+        case GTAP_E_CHILD_LIMIT: return "GTAP_E_CHILD_LIMIT";
+        case GTAP_E_TIMEOUT: return "GTAP_E_TIMEOUT";
+        case GTAP_E_BAD_STATE: return "GTAP_E_BAD_STATE";
+        case GTAP_E_NO_DEVICE: return "GTAP_E_NO_DEVICE";
+        case GTAP_E_UNSUPPORTED: return "GTAP_E_UNSUPPORTED";
+    }
+    return "GTAP_E_UNKNOWN";
+}
+
+gtap_status gtap_config_default(gtap_config* cfg, int32_t device, uint32_t kind) {
+    if (!cfg || kind > GTAP_WORKER_BLOCK) return GTAP_E_INVAL;
+    std::memset(cfg, 0, sizeof(*cfg));
+    cfg->struct_size = sizeof(gtap_config);
+    cfg->device = device;
+    cfg->worker_kind = kind;
+    cfg->block_size = (kind == GTAP_WORKER_THREAD) ? 128 : 256;
+    cfg->max_tasks_per_worker = (kind == GTAP_WORKER_THREAD) ? 4096 : 4096;
+    cfg->num_queues = 1;
+    cfg->steal_attempts = 4;
+    cfg->seed = 0x5EEDull;
+    return GTAP_OK;
+}
+
+size_t gtap_workspace_bytes(const gtap_config* in) {
+    gtap_config c;
+    const int sm = in ? device_sm_count(in->device) : 0;
+    if (resolve(in, &c, sm > 0 ? sm : 148) != GTAP_OK) return 0;
+    const uint32_t W = workers_alloc(c, sm > 0 ? sm : 148);
+    return gtap::make_layout(W, c.max_tasks_per_worker, c.queue_capacity, c.max_roots).total;
+}
+
+gtap_status gtap_init(const gtap_config* in, void* d_workspace, size_t bytes, gtap_runtime** out) {
+    if (!out) return GTAP_E_INVAL;
+    *out = nullptr;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return GTAP_E_NO_DEVICE;
+    if (!in || in->device < 0 || in->device >= ndev) return GTAP_E_INVAL;
+    int major = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, in->device);
+    if (major != 10) return GTAP_E_NO_DEVICE;  // built for sm_100a only
+    const int sm = device_sm_count(in->device);
+    gtap_config c;
+    gtap_status st = resolve(in, &c, sm);
+    if (st != GTAP_OK) return st;
+    if (cudaSetDevice(c.device) != cudaSuccess) return GTAP_E_CUDA;
+
+    gtap_runtime* rt = new (std::nothrow) gtap_runtime();
+    if (!rt) return GTAP_E_NOMEM;
+    rt->cfg = c;
+    rt->device = c.device;
+    rt->sm_count = sm;
+    rt->wpb = (c.worker_kind == GTAP_WORKER_THREAD) ? c.block_size / 32 : 1;
+    rt->W_alloc = workers_alloc(c, sm);
+    rt->M = c.max_tasks_per_worker;
+    rt->Q = c.queue_capacity;
+    rt->max_roots = c.max_roots;
+    rt->L = gtap::make_layout(rt->W_alloc, rt->M, rt->Q, rt->max_roots);
+    if (d_workspace) {
+        if (bytes < rt->L.total || ((uintptr_t)d_workspace & 255u)) { delete rt; return GTAP_E_INVAL; }
+        rt->ws = static_cast<char*>(d_workspace);
+        rt->owns_ws = false;
+    } else {
+        if (cudaMalloc(&rt->ws, rt->L.total) != cudaSuccess) { delete rt; return GTAP_E_NOMEM; }
+        rt->owns_ws = true;
+    }
+    if (cudaHostAlloc(&rt->h_roots, sizeof(RootSpec) * rt->max_roots, cudaHostAllocDefault) != cudaSuccess ||
+        cudaHostAlloc(&rt->h_ctl, sizeof(Ctl), cudaHostAllocDefault) != cudaSuccess) {
+        gtap_finalize(rt);
+        return GTAP_E_NOMEM;
+    }
+    if (cudaEventCreate(&rt->ev0) != cudaSuccess || cudaEventCreate(&rt->ev1) != cudaSuccess) {
+        gtap_finalize(rt);
+        return GTAP_E_CUDA;
+    }
+    rt->dirty = true;
+    if ((st = do_reset(rt, 0)) != GTAP_OK || cudaStreamSynchronize(0) != cudaSuccess) {
+        gtap_finalize(rt);
+        return st != GTAP_OK ? st : GTAP_E_CUDA;
+    }
+    *out = rt;
+    return GTAP_OK;
+}
+
+gtap_status gtap_spawn_root(gtap_runtime* rt, const gtap_task_table* t, uint32_t fn, const void* args,
+                            uint32_t nbytes, uint32_t* root_idx) {
+    if (!rt || !t || nbytes > sizeof(uint32_t) * gtap::kDataWords || (nbytes && !args)) return GTAP_E_INVAL;
+    if (rt->in_flight) return GTAP_E_BUSY;
+    if (t->kind != rt->cfg.worker_kind) return GTAP_E_INVAL;
+    if (rt->table && rt->table != t && !rt->roots.empty()) return GTAP_E_INVAL;  // one table per run
+    if (rt->roots.size() >= rt->max_roots) return GTAP_E_INVAL;
+    RootSpec r{};
+    r.fn = fn;
+    if (nbytes) std::memcpy(r.d, args, nbytes);  // firstprivate copy
+    if (fn >= t->nfn || (t->validate_root && t->validate_root(t, fn, r.d) != 0)) return GTAP_E_INVAL;
+    rt->table = t;
+    if (root_idx) *root_idx = (uint32_t)rt->roots.size();
+    rt->roots.push_back(r);
+    return GTAP_OK;
+}
+
+gtap_status gtap_reset(gtap_runtime* rt, void* stream) {
+    if (!rt) return GTAP_E_INVAL;
+    if (rt->in_flight) return GTAP_E_BUSY;
+    rt->roots.clear();
+    rt->table = nullptr;
+    return do_reset(rt, static_cast<cudaStream_t>(stream));
+}
+
+gtap_status gtap_geometry(gtap_runtime* rt, const gtap_task_table* t, uint32_t* workers, uint32_t* grid,
+                          uint32_t* block) {
+    if (!rt || !t) return GTAP_E_INVAL;
+    cudaSetDevice(rt->device);
+    uint32_t W = 0, g = 0, b = 0;
+    gtap_status st = geometry(rt, t, &W, &g, &b);
+    if (st != GTAP_OK) return st;
+    if (workers) *workers = W;
+    if (grid) *grid = g;
+    if (block) *block = b;
+    return GTAP_OK;
+}
+
+gtap_status gtap_run(gtap_runtime* rt, void* stream) {
+    if (!rt) return GTAP_E_INVAL;
+    if (rt->in_flight) return GTAP_E_BUSY;
+    if (rt->roots.empty() || !rt->table) return GTAP_E_INVAL;
+    cudaSetDevice(rt->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    uint32_t W = 0, grid = 0, block = 0;
+    gtap_status st = geometry(rt, rt->table, &W, &grid, &block);
+    if (st != GTAP_OK) return st;
+    if (rt->dirty && (st = do_reset(rt, s)) != GTAP_OK) return st;
+    const uint32_t nroots = (uint32_t)rt->roots.size();
+    // roots + termination counters: one pinned H2D copy each
+    std::memcpy(rt->h_roots, rt->roots.data(), sizeof(RootSpec) * nroots);
+    if (cudaMemcpyAsync(rt->ws + rt->L.roots, rt->h_roots, sizeof(RootSpec) * nroots, cudaMemcpyHostToDevice, s) !=
+        cudaSuccess)
+        return GTAP_E_CUDA;
+    std::memset(rt->h_ctl, 0, sizeof(Ctl));
+    rt->h_ctl->roots_left = nroots;
+    rt->h_ctl->outstanding = nroots;
+    if (cudaMemcpyAsync(rt->ws + rt->L.ctl, rt->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, s) != cudaSuccess)
+        return GTAP_E_CUDA;
+
+    KParams p{};
+    p.W = W;
+    p.logM = log2u(rt->M);
+    p.qmask = rt->Q - 1u;
+    p.steal_rounds = rt->cfg.steal_attempts;
+    p.steal_max = rt->cfg.steal_max;
+    p.nroots = nroots;
+    p.max_child = rt->cfg.max_child_tasks ? rt->cfg.max_child_tasks : rt->table->max_children;
+    p.seed = rt->cfg.seed;
+    p.watchdog_ns = rt->cfg.watchdog_ns;
+    p.rec = reinterpret_cast<gtap::TaskRec*>(rt->ws + rt->L.rec);
+    p.ring = reinterpret_cast<uint32_t*>(rt->ws + rt->L.ring);
+    p.dq = reinterpret_cast<gtap::DequeMeta*>(rt->ws + rt->L.dq);
+    p.fring = reinterpret_cast<uint32_t*>(rt->ws + rt->L.fring);
+    p.fm = reinterpret_cast<gtap::FreeMeta*>(rt->ws + rt->L.fm);
+    p.ctl = reinterpret_cast<Ctl*>(rt->ws + rt->L.ctl);
+    p.roots = reinterpret_cast<const RootSpec*>(rt->ws + rt->L.roots);
+    p.root_results = reinterpret_cast<long long*>(rt->ws + rt->L.results);
+
+    if (cudaEventRecord(rt->ev0, s) != cudaSuccess) return GTAP_E_CUDA;
+    const cudaError_t le = rt->table->launch(rt->table, p, grid, block, s);
+    if (le != cudaSuccess) return GTAP_E_CUDA;
+    if (cudaEventRecord(rt->ev1, s) != cudaSuccess) return GTAP_E_CUDA;
+    rt->in_flight = true;
+    rt->dirty = true;
+    rt->run_grid = grid;
+    rt->run_block = block;
+    rt->run_W = W;
+    rt->run_nroots = nroots;
+    rt->roots.clear();
+    return GTAP_OK;
+}
+
+gtap_status gtap_sync(gtap_runtime* rt, gtap_stats* out) {
+    if (!rt) return GTAP_E_INVAL;
+    if (!rt->in_flight) return GTAP_E_INVAL;
+    cudaSetDevice(rt->device);
+    rt->in_flight = false;
+    if (cudaEventSynchronize(rt->ev1) != cudaSuccess) return GTAP_E_CUDA;
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, rt->ev0, rt->ev1);
+    if (cudaMemcpy(rt->h_ctl, rt->ws + rt->L.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost) != cudaSuccess)
+        return GTAP_E_CUDA;
+    const Ctl& c = *rt->h_ctl;
+    if (out) {
+        std::memset(out, 0, sizeof(*out));
+        out->tasks = c.stats[gtap::ST_TASKS];
+        out->invocations = c.stats[gtap::ST_INVOC];
+        out->pops = c.stats[gtap::ST_POPS];
+        out->kept = c.stats[gtap::ST_KEPT];
+        out->steals_ok = c.stats[gtap::ST_STEALS_OK];
+        out->steals_failed = c.stats[gtap::ST_STEALS_FAILED];
+        out->stolen_tasks = c.stats[gtap::ST_STOLEN];
+        out->pushes = c.stats[gtap::ST_PUSHES];
+        out->cycles = c.stats[gtap::ST_CYCLES];
+        out->idle_cycles = c.stats[gtap::ST_IDLE];
+        out->remote_frees = c.stats[gtap::ST_REMOTE_FREES];
+        out->max_pool_used = c.stats[gtap::ST_MAX_POOL];
+        out->error_word = c.error;
+        out->workers = rt->run_W;
+        out->device_ms = ms;
+        out->grid_size = rt->run_grid;
+        out->block_size = rt->run_block;
+    }
+    if (c.error) return static_cast<gtap_status>(c.error);
+    if (!c.done) return GTAP_E_BAD_STATE;  // kernel exited without termination (should not happen)
+    return GTAP_OK;
+}
+
+gtap_status gtap_root_result(gtap_runtime* rt, uint32_t root_idx, void* out, uint32_t nbytes) {
+    if (!rt || !out || nbytes > 8) return GTAP_E_INVAL;
+    if (rt->in_flight) return GTAP_E_BUSY;
+    if (root_idx >= rt->run_nroots) return GTAP_E_INVAL;
+    cudaSetDevice(rt->device);
+    long long v = 0;
+    if (cudaMemcpy(&v, rt->ws + rt->L.results + sizeof(long long) * root_idx, sizeof(v), cudaMemcpyDeviceToHost) !=
+        cudaSuccess)
+        return GTAP_E_CUDA;
+    std::memcpy(out, &v, nbytes);
+    return GTAP_OK;
+}
+
+gtap_status gtap_finalize(gtap_runtime* rt) {
+    if (!rt) return GTAP_OK;
+    cudaSetDevice(rt->device);
+    if (rt->in_flight) cudaEventSynchronize(rt->ev1);
+    if (rt->owns_ws && rt->ws) cudaFree(rt->ws);
+    if (rt->h_roots) cudaFreeHost(rt->h_roots);
+    if (rt->h_ctl) cudaFreeHost(rt->h_ctl);
+    if (rt->ev0) cudaEventDestroy(rt->ev0);
+    if (rt->ev1) cudaEventDestroy(rt->ev1);
+    delete rt;
+    return GTAP_OK;
+}
+
+void gtap_table_destroy(const gtap_task_table* t) { delete const_cast<gtap_task_table*>(t); }
+
+}  // extern "C"

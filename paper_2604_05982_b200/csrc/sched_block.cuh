@@ -1,0 +1,422 @@
+// sched_block.cuh -- block-level persistent scheduler ("block-cooperative"
+// mode, §4.1; deque §4.3.1; API §5.1.3).
+//
+// One worker = one thread block. Warp 0 is the queue leader ("a
+// designated leader thread performs queue operations, and each pop/steal
+// retrieves at most one task"): it takes the kept task or pops one task from
+// the block's own deque, else steals one (probing 32 random victims in
+// parallel, one per lane), and broadcasts the record through shared memory.
+// All threads then run the task body data-parallel (threadIdx/blockDim,
+// __syncthreads, shared memory: P:1081-1082). Spawns made by individual
+// threads ("performed by the thread that reaches the pragma") are
+// staged in shared memory (reading R13) and published by warp 0 after the
+// body, or mid-body through flush() for tables without taskwait.
+//
+// The deque is the same split ring as the thread-level one (DESIGN.md
+// "Deque") with claims of exactly one task, i.e. a fixed-capacity Chase-Lev
+// deque whose owner end is private until published.
+#pragma once
+#include "gtap.h"
+#include "gtap_internal.cuh"
+
+namespace gtap {
+
+struct ChildSpec {
+    uint32_t fn;
+    uint32_t d[kDataWords];
+};
+
+template <class T>
+struct BlockSmem {
+    uint32_t task_id;         // task of this cycle (kNone: none)
+    uint32_t exit_flag;
+    uint32_t fn, state, parent, aux, ord;
+    uint32_t d[kDataWords];
+    uint32_t nspawn;          // staged children (smem atomic)
+    uint32_t action;          // 1 finish, 2 suspend
+    uint32_t next_state;
+    uint32_t has_result;
+    int32_t result;
+    uint32_t err;
+    ChildSpec spawns[T::kSpawnCap];
+    typename T::Scratch scratch;
+};
+
+// Leader-side (warp 0) persistent state.
+struct BLeader {
+    uint32_t tail, split, sdone, bump, fhead, kept, rng, backoff;
+    unsigned long long st[ST_COUNT];
+};
+
+template <class T>
+struct BCtx;
+template <class T>
+__device__ void block_flush(BlockSmem<T>& sm, const KParams& p, BLeader& L, uint32_t w, uint32_t headroom);
+
+template <class T>
+struct BCtx {
+    BlockSmem<T>& sm;
+    const KParams& p;
+    BLeader& L;
+    uint32_t w;
+    __device__ __forceinline__ BCtx(BlockSmem<T>& s, const KParams& pp, BLeader& l, uint32_t ww)
+        : sm(s), p(pp), L(l), w(ww) {}
+    // uniform: publish staged spawns if fewer than `headroom` staging slots remain (no-taskwait tables only)
+    __device__ __forceinline__ void flush(uint32_t headroom) { block_flush<T>(sm, p, L, w, headroom); }
+    // called by any subset of threads (the ones that reach the spawn)
+    __device__ __forceinline__ void spawn(uint32_t fn, uint32_t d0, uint32_t d1 = 0, uint32_t d2 = 0, uint32_t d3 = 0) {
+        const uint32_t i = atomicAdd(&sm.nspawn, 1u);
+        if (i < (uint32_t)T::kSpawnCap) {
+            ChildSpec& c = sm.spawns[i];
+            c.fn = fn; c.d[0] = d0; c.d[1] = d1; c.d[2] = d2; c.d[3] = d3;
+        } else {
+            atomicCAS(&sm.err, 0u, (uint32_t)GTAP_E_CHILD_LIMIT);
+        }
+    }
+    // single-thread (thread 0) or uniform calls
+    __device__ __forceinline__ void finish(int32_t r) { sm.action = 1; sm.has_result = 1; sm.result = r; }
+    __device__ __forceinline__ void finish_void() { sm.action = 1; }
+    __device__ __forceinline__ void suspend(uint32_t next) { sm.action = 2; sm.next_state = next; }
+    __device__ __forceinline__ void bad_state() { sm.action = 1; sm.err = GTAP_E_BAD_STATE; }
+};
+
+// warp 0: draw `cnt` (<= 32) record IDs from the own pool into out[] (lane i gets out[i]).
+// Returns false (and raises) on exhaustion.
+__device__ __forceinline__ bool block_alloc(const KParams& p, BLeader& L, uint32_t w, uint32_t lane, uint32_t cnt,
+                                            uint32_t& id_out) {
+    using namespace dev;
+    const uint32_t M = 1u << p.logM, mmask = M - 1u;
+    uint32_t* myfring = p.fring + ((size_t)w << p.logM);
+    uint32_t e = 0;
+    if (lane < cnt) e = ld_relaxed(&myfring[(L.fhead + lane) & mmask]);
+    const uint32_t valid = __ballot_sync(0xffffffffu, e != 0u);
+    const uint32_t k = min((uint32_t)(__ffs(~valid) - 1), cnt);
+    if (lane < k) {
+        id_out = e - 1u;
+        st_relaxed(&myfring[(L.fhead + lane) & mmask], 0u);
+    }
+    L.fhead += k;
+    const uint32_t rest = cnt - k;
+    if (rest) {
+        if (L.bump + rest > M) {
+            if (lane == 0) raise_error(p.ctl, GTAP_E_POOL_EXHAUSTED);
+            return false;
+        }
+        if (lane >= k && lane < cnt) id_out = (w << p.logM) + L.bump + (lane - k);
+        L.bump += rest;
+    }
+    return true;
+}
+
+// warp 0: free record `id` (lane-predicated `doit`) to its home free ring.
+__device__ __forceinline__ void block_free(const KParams& p, uint32_t lane, bool doit, uint32_t id) {
+    using namespace dev;
+    const uint32_t mask = __ballot_sync(0xffffffffu, doit);
+    if (!doit) return;
+    const uint32_t home = id >> p.logM;
+    const uint32_t grp = __match_any_sync(mask, home);
+    const uint32_t leader = __ffs(grp) - 1u;
+    uint32_t base = 0;
+    if (lane == leader) base = atom_add_relaxed(&p.fm[home].tail, (uint32_t)__popc(grp));
+    base = __shfl_sync(grp, base, leader);
+    const uint32_t slot = base + __popc(grp & lanemask_lt());
+    st_relaxed(&p.fring[((size_t)home << p.logM) + (slot & ((1u << p.logM) - 1u))], id + 1u);
+}
+
+// warp 0: move staged children [0, cnt) into records and onto the deque.
+// keep_last: keep the newest child for the next cycle instead of pushing it.
+template <class T>
+__device__ bool block_publish_spawns(const KParams& p, BLeader& L, BlockSmem<T>& sm, uint32_t w, uint32_t lane,
+                                     uint32_t cnt, uint32_t parent_id, bool keep_last, bool count_outstanding) {
+    using namespace dev;
+    const uint32_t Q = p.qmask + 1u;
+    uint32_t* ring = p.ring + (size_t)w * Q;
+    if (cnt == 0) return true;
+    if (!T::kTaskwait && count_outstanding) {
+        // outstanding += children before any of them can be published (termination, R6)
+        if (lane == 0) atom_add_acq_rel(&p.ctl->outstanding, (long long)cnt);
+    }
+    uint32_t pushc = keep_last ? cnt - 1u : cnt;
+    if (pushc && L.tail + pushc - L.sdone > Q) {
+        if (lane == 0) L.sdone = ld_relaxed(&p.dq[w].steal_done);
+        L.sdone = __shfl_sync(0xffffffffu, L.sdone, 0);
+        if (L.tail + pushc - L.sdone > Q) {
+            if (lane == 0) raise_error(p.ctl, GTAP_E_QUEUE_OVERFLOW);
+            return false;
+        }
+    }
+    for (uint32_t b = 0; b < cnt; b += 32) {
+        const uint32_t c = min(32u, cnt - b);
+        uint32_t id = kNone;
+        if (!block_alloc(p, L, w, lane, c, id)) return false;
+        if (lane < c) {
+            const ChildSpec cs = sm.spawns[b + lane];
+            TaskRec* r = p.rec + id;
+            st_v4(r, make_uint4(make_meta(cs.fn, 0, b + lane, 0), 0u, parent_id, 0u));
+            st_v4(&r->d[0], make_uint4(cs.d[0], cs.d[1], cs.d[2], cs.d[3]));
+            const uint32_t i = b + lane;
+            if (keep_last && i == cnt - 1u) L.kept = id;  // lane-local; broadcast below
+            else ring[(L.tail + i) & p.qmask] = id;
+        }
+        if (keep_last && cnt - 1u >= b && cnt - 1u < b + c) {
+            L.kept = __shfl_sync(0xffffffffu, L.kept, (cnt - 1u) - b);
+        }
+    }
+    L.tail += pushc;
+    if (lane == 0) L.st[ST_TASKS] += cnt, L.st[ST_PUSHES] += pushc;
+    return true;
+}
+
+// warp 0: publish half of the private part if thieves drained the public part.
+__device__ __forceinline__ void block_maybe_publish(const KParams& p, BLeader& L, uint32_t w, uint32_t lane) {
+    using namespace dev;
+    if (lane == 0) {
+        const unsigned long long s = ld_relaxed(&p.dq[w].S);
+        const uint32_t priv = L.tail - L.split;
+        if ((uint32_t)s == L.split && priv >= 2u) {
+            const uint32_t k = priv >> 1;
+            L.split += k;
+            red_add_release(&p.dq[w].S, (unsigned long long)k << 32);
+        }
+    }
+    L.split = __shfl_sync(0xffffffffu, L.split, 0);
+}
+
+template <class T>
+__global__ void __launch_bounds__(1024) block_sched_kernel(KParams p, typename T::Args args) {
+    using namespace dev;
+    __shared__ BlockSmem<T> sm;
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    const uint32_t w = blockIdx.x;
+    if (w >= p.W) return;
+    const uint32_t Q = p.qmask + 1u, qmask = p.qmask;
+    uint32_t* ring = p.ring + (size_t)w * Q;
+    DequeMeta* mydq = p.dq + w;
+    BLeader L;
+    BCtx<T> ctx(sm, p, L, w);
+    const unsigned long long t0 = globaltimer();
+
+    if (warp == 0) {
+        L.tail = L.split = L.sdone = L.bump = L.fhead = 0;
+        L.kept = kNone;
+        L.backoff = 64;
+        L.rng = hash32(p.seed * 0x9E3779B97F4A7C15ull + (unsigned long long)w * 32u + lane);
+#pragma unroll
+        for (int i = 0; i < ST_COUNT; ++i) L.st[i] = 0;
+        // entry: roots w, w + W, ... onto this block's deque
+        uint32_t mine = p.nroots > w ? (p.nroots - w + p.W - 1) / p.W : 0;
+        if (mine > (1u << p.logM) || mine > Q) {
+            if (lane == 0) raise_error(p.ctl, GTAP_E_POOL_EXHAUSTED);
+            mine = 0;
+        }
+        for (uint32_t i = lane; i < mine; i += 32) {
+            const uint32_t r = w + i * p.W;
+            const RootSpec rs = p.roots[r];
+            const uint32_t id = (w << p.logM) + i;
+            TaskRec* rec = p.rec + id;
+            st_v4(rec, make_uint4(make_meta(rs.fn, 0, 0, 0), 0u, kNone, kRootFlag | r));
+            st_v4(&rec->d[0], make_uint4(rs.d[0], rs.d[1], rs.d[2], rs.d[3]));
+            ring[i & qmask] = id;
+        }
+        L.bump = mine;
+        L.tail = mine;
+        if (lane == 0) L.st[ST_TASKS] += mine;
+        __syncwarp();
+    }
+    if (tid == 0) { sm.exit_flag = 0; }
+
+    while (true) {
+        // ================= warp 0: acquire one task =================
+        if (warp == 0) {
+            uint32_t id = kNone;
+            if (L.kept != kNone) {
+                id = L.kept;
+                L.kept = kNone;
+                if (lane == 0) ++L.st[ST_KEPT];
+            } else if (L.tail != L.split) {  // LIFO pop, private part
+                L.tail -= 1u;
+                if (lane == 0) id = ld_relaxed(&ring[L.tail & qmask]);
+                id = __shfl_sync(0xffffffffu, id, 0);
+                if (lane == 0) ++L.st[ST_POPS];
+            } else {
+                // reclaim one from the own public part
+                uint32_t got = kNone;
+                if (lane == 0) {
+                    unsigned long long s = ld_relaxed(&mydq->S);
+                    for (int it = 0; it < 8; ++it) {
+                        const uint32_t h = (uint32_t)s, sp = (uint32_t)(s >> 32);
+                        if (sp == h || sp - h > Q) break;
+                        const unsigned long long nw = ((unsigned long long)(sp - 1u) << 32) | h;
+                        const unsigned long long o = atom_cas_relaxed(&mydq->S, s, nw);
+                        if (o == s) { got = ld_relaxed(&ring[(sp - 1u) & qmask]); L.split = sp - 1u; break; }
+                        s = o;
+                    }
+                }
+                L.split = __shfl_sync(0xffffffffu, L.split, 0);
+                L.tail = L.split;
+                id = __shfl_sync(0xffffffffu, got, 0);
+                if (id != kNone && lane == 0) ++L.st[ST_POPS];
+                // steal one from the fullest of 32 random victims
+                for (uint32_t round = 0; id == kNone && round < p.steal_rounds && p.W > 1; ++round) {
+                    uint32_t v = xorshift32(L.rng) % (p.W - 1u);
+                    v += (v >= w);
+                    const unsigned long long sv = ld_relaxed(&p.dq[v].S);
+                    uint32_t avail = (uint32_t)(sv >> 32) - (uint32_t)sv;
+                    if (avail > Q) avail = 0;
+                    uint32_t best = (min(avail, (1u << 26)) << 5) | lane;
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+                    if ((best >> 5) == 0) { if (lane == 0) ++L.st[ST_STEALS_FAILED]; continue; }
+                    const uint32_t victim = __shfl_sync(0xffffffffu, v, best & 31u);
+                    DequeMeta* vdq = p.dq + victim;
+                    uint32_t sid = kNone;
+                    if (lane == 0 && atom_cas_relaxed(&vdq->lock, 0u, 1u) == 0u) {
+                        unsigned long long s = ld_relaxed(&vdq->S);
+                        for (int it = 0; it < 8; ++it) {
+                            const uint32_t h = (uint32_t)s, sp = (uint32_t)(s >> 32);
+                            if (sp == h || sp - h > Q) break;
+                            const unsigned long long nw = ((unsigned long long)sp << 32) | (uint32_t)(h + 1u);
+                            const unsigned long long o = atom_cas_acquire(&vdq->S, s, nw);
+                            if (o == s) { sid = ld_relaxed(&p.ring[(size_t)victim * Q + (h & qmask)]); break; }
+                            s = o;
+                        }
+                        if (sid != kNone) red_add_release(&vdq->steal_done, 1u);
+                        st_relaxed(&vdq->lock, 0u);
+                    }
+                    id = __shfl_sync(0xffffffffu, sid, 0);
+                    if (lane == 0) { if (id != kNone) { ++L.st[ST_STEALS_OK]; ++L.st[ST_STOLEN]; } else ++L.st[ST_STEALS_FAILED]; }
+                }
+            }
+            if (id != kNone) {
+                if (lane == 0) {
+                    const uint4 h = ld_relaxed_v4(p.rec + id);
+                    const uint4 dv = ld_relaxed_v4(&p.rec[id].d[0]);
+                    sm.fn = meta_fn(h.x); sm.state = meta_state(h.x); sm.ord = meta_ord(h.x);
+                    sm.parent = h.z; sm.aux = h.w;
+                    sm.d[0] = dv.x; sm.d[1] = dv.y; sm.d[2] = dv.z; sm.d[3] = dv.w;
+                    sm.nspawn = 0; sm.action = 0; sm.has_result = 0; sm.err = 0;
+                    ++L.st[ST_CYCLES];
+                    ++L.st[ST_INVOC];
+                }
+                L.backoff = 64;
+            } else {
+                if (lane == 0) ++L.st[ST_IDLE];
+                uint32_t d = 0;
+                if (lane == 0) {
+                    d = ld_relaxed(&p.ctl->done);
+                    if (!d && p.watchdog_ns && globaltimer() - t0 > p.watchdog_ns) raise_error(p.ctl, GTAP_E_TIMEOUT);
+                }
+                d = __shfl_sync(0xffffffffu, d, 0);
+                if (d && lane == 0) sm.exit_flag = 1;
+                if (!d) {
+                    nanosleep(L.backoff);
+                    L.backoff = min(L.backoff * 2u, 2048u);
+                }
+            }
+            if (lane == 0) sm.task_id = id;
+        }
+        __syncthreads();
+        if (sm.exit_flag) break;
+        const uint32_t my = sm.task_id;
+        if (my == kNone) continue;
+
+        // ================= all threads: run the task body =================
+        {
+            const uint32_t d[kDataWords] = {sm.d[0], sm.d[1], sm.d[2], sm.d[3]};
+            T::exec_block(args, ctx, sm.fn, sm.state, d);
+        }
+        __syncthreads();
+
+        // ================= warp 0: spawn / join / finish =================
+        if (warp == 0) {
+            const uint32_t err = sm.err ? sm.err : (sm.action == 0 ? (uint32_t)GTAP_E_BAD_STATE : 0u);
+            const uint32_t staged = min(sm.nspawn, (uint32_t)T::kSpawnCap);
+            bool ok = (err == 0u);
+            if (!ok && lane == 0) raise_error(p.ctl, err);
+            const bool fin = (sm.action == 1);
+            const uint32_t total_children = staged;
+            if (ok && !T::kTaskwait && lane == 0) {
+                // one atomic per task: +children (before they are published) -1 for this task (R6)
+                const long long delta = (long long)staged - 1ll;
+                if (delta != 0) {
+                    const long long old = atom_add_acq_rel(&p.ctl->outstanding, delta);
+                    if (old + delta == 0) st_release(&p.ctl->done, 1u);
+                }
+            }
+            if (ok) {
+                // a resumed parent takes the kept slot later; the kept child is then pushed
+                ok = block_publish_spawns<T>(p, L, sm, w, lane, staged, T::kTaskwait ? my : kNone, true, false);
+            }
+            if (ok) {
+                if (sm.action == 2) {
+                    // suspend: resumption state + join counter
+                    if (lane == 0) st_v2(p.rec + my, make_meta(sm.fn, sm.next_state, sm.ord, 0), total_children);
+                    if (total_children == 0u) {
+                        if (L.kept != kNone) {  // keep the continuation, push the kept child instead
+                            if (lane == 0) ring[L.tail & qmask] = L.kept;
+                            L.tail += 1u;
+                        }
+                        L.kept = my;
+                    }
+                } else if (fin) {
+                    const uint32_t parent = sm.parent;
+                    if (parent != kNone && sm.has_result && lane == 0)
+                        st_relaxed(reinterpret_cast<int32_t*>(&p.rec[parent].d[2 + sm.ord]), sm.result);
+                    block_free(p, lane, lane == 0, my);
+                    __syncwarp();
+                    uint32_t resume = kNone;
+                    if (lane == 0) {
+                        if (parent != kNone) {
+                            if (atom_add_acq_rel(&p.rec[parent].pending, -1) == 1) resume = parent;
+                        } else if (sm.aux & kRootFlag) {
+                            p.root_results[sm.aux & ~kRootFlag] = sm.has_result ? (long long)sm.result : 0ll;
+                            if (T::kTaskwait && atom_add_acq_rel(&p.ctl->roots_left, 0xFFFFFFFFu) == 1u)
+                                st_release(&p.ctl->done, 1u);
+                        }
+                    }
+                    resume = __shfl_sync(0xffffffffu, resume, 0);
+                    if (resume != kNone) {
+                        if (L.kept != kNone) {
+                            if (lane == 0) ring[L.tail & qmask] = L.kept;
+                            L.tail += 1u;
+                        }
+                        L.kept = resume;
+                    }
+                }
+                block_maybe_publish(p, L, w, lane);
+            }
+            __syncwarp();
+        }
+        // (next iteration's acquire runs in warp 0; other warps wait at the barrier above)
+    }
+
+    if (warp == 0 && lane == 0) {
+        unsigned long long* s = p.ctl->stats;
+        for (int i = 0; i < ST_COUNT; ++i)
+            if (i != ST_MAX_POOL && L.st[i]) atomicAdd(&s[i], L.st[i]);
+        atomicMax(&s[ST_MAX_POOL], (unsigned long long)L.bump);
+    }
+}
+
+// Mid-body flush for tables without taskwait: publish staged spawns when the
+// staging buffer could overflow in the next chunk. Must be called uniformly
+// by all threads of the block.
+template <class T>
+__device__ void block_flush(BlockSmem<T>& sm, const KParams& p, BLeader& L, uint32_t w,
+                                            uint32_t headroom) {
+    static_assert(!T::kTaskwait, "mid-body flush would publish children before the join count is set");
+    __syncthreads();
+    const uint32_t staged = sm.nspawn;
+    if (staged + headroom > (uint32_t)T::kSpawnCap) {
+        if ((threadIdx.x >> 5) == 0) {
+            const uint32_t lane = threadIdx.x & 31u;
+            block_publish_spawns<T>(p, L, sm, w, lane, min(staged, (uint32_t)T::kSpawnCap), kNone, false, true);
+            block_maybe_publish(p, L, w, lane);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) sm.nspawn = 0;
+        __syncthreads();
+    }
+}
+
+}  // namespace gtap

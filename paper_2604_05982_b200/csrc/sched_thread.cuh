@@ -1,0 +1,429 @@
+// sched_thread.cuh -- thread-level persistent scheduler ("thread-executed"
+// mode, §4.1; queue design §4.3.2).
+//
+// One worker = one warp. Each persistent-kernel cycle a warp
+//   (1) acquires up to 32 runnable task IDs: the set kept from its previous
+//       cycle, then a LIFO batch from its own deque, then (only if still
+//       empty) a FIFO batch stolen from a random victim;
+//   (2) executes them, one task per lane, as switch-on-state functions
+//       (P:52-55): exec() returns spawn requests + finish/suspend;
+//   (3) allocates child records from the warp's pool, joins (atomic pending
+//       decrement, last child re-enqueues the parent), keeps up to 32
+//       runnable tasks for the next cycle and pushes the rest, and
+//       publishes part of its private deque when thieves have drained the
+//       public part.
+//
+// Deque (B200 design): a power-of-two ring per warp in HBM
+// with a packed 64-bit word S = head | split << 32. The owner pushes and pops
+// at the tail of the PRIVATE part [split, tail) with no atomics at all (tail
+// and split live in registers -- only the owner moves them).
+// Thieves CAS S to claim [head, head + c) of the PUBLIC part [head, split)
+// under a per-victim try-lock; the owner publishes the oldest
+// half of its private part with one red.release when it sees the public part
+// empty, and reclaims from the public part by CAS only when its private part
+// and kept set are empty. This keeps the paper's batched claim-by-CAS for
+// steals but moves the owner's common-case pop off the shared counter
+// whose contention the paper identifies as its scaling limit.
+#pragma once
+#include "gtap.h"
+#include "gtap_internal.cuh"
+
+namespace gtap {
+
+// What one thread-level invocation produced (the runtime side of
+// __gtap_prepare_for_join / __gtap_finish_task).
+template <int MAXC>
+struct TOut {
+    uint32_t action;      // 0 = none, 1 = finish, 2 = suspend
+    uint32_t nchild;
+    uint32_t next_state;
+    uint32_t has_result;
+    int32_t result;
+    uint32_t err;
+    uint32_t cfn[MAXC];
+    uint32_t cd[MAXC][kDataWords];
+    static constexpr uint32_t kFinish = 1, kSuspend = 2;
+    __device__ __forceinline__ void init() { action = 0; nchild = 0; has_result = 0; err = 0; result = 0; next_state = 0; }
+    // spawn child #i (i is a compile-time constant after inlining)
+    __device__ __forceinline__ void spawn(int i, uint32_t fn, uint32_t d0, uint32_t d1 = 0, uint32_t d2 = 0,
+                                          uint32_t d3 = 0) {
+        if (i >= MAXC) { err = GTAP_E_CHILD_LIMIT; return; }
+        cfn[i] = fn; cd[i][0] = d0; cd[i][1] = d1; cd[i][2] = d2; cd[i][3] = d3;
+        nchild = (uint32_t)i + 1 > nchild ? (uint32_t)i + 1 : nchild;
+    }
+    __device__ __forceinline__ void suspend(uint32_t next) { action = kSuspend; next_state = next; }
+    __device__ __forceinline__ void finish(int32_t r) { action = kFinish; has_result = 1; result = r; }
+    __device__ __forceinline__ void finish_void() { action = kFinish; }
+    __device__ __forceinline__ void bad_state() { action = kFinish; err = GTAP_E_BAD_STATE; }
+};
+
+template <int MAXC>
+struct WarpSmem {
+    uint32_t kept[32];          // keep-for-next-cycle set
+    uint32_t fbuf[32];          // records freed this cycle (reused first)
+    uint32_t abuf[32 * MAXC];   // records drawn from the free ring / bump region
+    uint32_t cbuf[32 * MAXC];   // child IDs spawned this cycle, spawn order
+    uint32_t pbuf[32];          // parents made runnable this cycle
+};
+
+template <class T>
+__global__ void __launch_bounds__(1024) thread_sched_kernel(KParams p, typename T::Args args) {
+    using namespace dev;
+    constexpr int MAXC = T::kMaxChildren;
+    using Out = TOut<MAXC>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t wib = threadIdx.x >> 5;
+    const uint32_t w = blockIdx.x * (blockDim.x >> 5) + wib;
+    if (w >= p.W) return;  // whole warp
+    WarpSmem<MAXC>& sm = reinterpret_cast<WarpSmem<MAXC>*>(smem_raw)[wib];
+
+    const uint32_t M = 1u << p.logM, mmask = M - 1u;
+    const uint32_t Q = p.qmask + 1u, qmask = p.qmask;
+    uint32_t* ring = p.ring + (size_t)w * Q;
+    DequeMeta* mydq = p.dq + w;
+    uint32_t* myfring = p.fring + ((size_t)w << p.logM);
+    const uint32_t base_id = w << p.logM;
+    const uint32_t lt = lanemask_lt();
+
+    // owner-local deque / pool state (warp-uniform, in registers)
+    uint32_t tail = 0, split = 0, sdone = 0;
+    uint32_t bump = 0, fhead = 0;
+    uint32_t nkept = 0;
+    uint32_t rng = hash32(p.seed * 0x9E3779B97F4A7C15ull + (unsigned long long)w * 32u + lane);
+    uint32_t backoff = 32;
+    unsigned long long st_tasks = 0, st_inv = 0, st_pops = 0, st_kept = 0, st_sok = 0, st_sfail = 0,
+                       st_stolen = 0, st_push = 0, st_cyc = 0, st_idle = 0, st_rfree = 0;
+    const unsigned long long t0 = globaltimer();
+    uint32_t cyc_u = 0;  // warp-uniform cycle counter (every lane increments it)
+    bool failed = false;
+
+    // ---- entry: roots r = w, w + W, ... go to this warp's deque
+    {
+        uint32_t mine = p.nroots > w ? (p.nroots - w + p.W - 1) / p.W : 0;
+        if (mine > M || mine > Q) {
+            if (lane == 0) raise_error(p.ctl, GTAP_E_POOL_EXHAUSTED);
+            mine = 0;
+        }
+        for (uint32_t i = lane; i < mine; i += 32) {
+            const uint32_t r = w + i * p.W;
+            const RootSpec rs = p.roots[r];
+            const uint32_t id = base_id + i;
+            TaskRec* rec = p.rec + id;
+            st_v4(rec, make_uint4(make_meta(rs.fn, 0, 0, 0), 0u, kNone, kRootFlag | r));
+            st_v4(&rec->d[0], make_uint4(rs.d[0], rs.d[1], rs.d[2], rs.d[3]));
+            ring[i & qmask] = id;
+        }
+        bump = mine;
+        tail = mine;
+        st_tasks += (lane == 0) ? mine : 0;
+        __syncwarp();
+    }
+
+    while (true) {
+        // ================= (1) acquire =================
+        uint32_t n = nkept;
+        uint32_t my = (lane < n) ? sm.kept[lane] : kNone;
+        unsigned long long S_seen = 0;
+        uint32_t done_seen = 0;
+        if (lane == 0) {
+            S_seen = ld_relaxed(&mydq->S);
+            done_seen = ld_relaxed(&p.ctl->done);
+        }
+        if (lane == 0) st_kept += n;
+        // LIFO pop from the private part: no atomics (owner only)
+        {
+            const uint32_t priv = tail - split;
+            if (n < 32 && priv > 0) {
+                const uint32_t c = min(32u - n, priv);
+                if (lane >= n && lane < n + c) my = ld_relaxed(&ring[(tail - 1u - (lane - n)) & qmask]);
+                tail -= c;
+                n += c;
+                if (lane == 0) st_pops += c;
+            }
+        }
+        // reclaim from the own public part (only when nothing else to run)
+        if (n == 0) {
+            uint32_t got = 0, s_new = 0;
+            if (lane == 0) {
+                unsigned long long s = S_seen;
+                for (int it = 0; it < 8; ++it) {
+                    const uint32_t h = (uint32_t)s, sp = (uint32_t)(s >> 32);
+                    const uint32_t avail = sp - h;
+                    if (avail == 0u || avail > Q) break;
+                    const uint32_t c = min(32u, avail);
+                    const unsigned long long nw = ((unsigned long long)(sp - c) << 32) | h;
+                    const unsigned long long o = atom_cas_relaxed(&mydq->S, s, nw);
+                    if (o == s) { got = c; s_new = sp - c; break; }
+                    s = o;
+                }
+            }
+            got = __shfl_sync(0xffffffffu, got, 0);
+            s_new = __shfl_sync(0xffffffffu, s_new, 0);
+            if (got) {
+                split = s_new;
+                tail = s_new;
+                if (lane < got) my = ld_relaxed(&ring[(s_new + got - 1u - lane) & qmask]);
+                n = got;
+                if (lane == 0) st_pops += got;
+            }
+        }
+        // steal: probe 32 random victims in parallel, claim from the fullest
+        if (n == 0 && p.W > 1) {
+            for (uint32_t round = 0; round < p.steal_rounds && n == 0; ++round) {
+                uint32_t v = xorshift32(rng) % (p.W - 1u);
+                v += (v >= w);
+                const unsigned long long sv = ld_relaxed(&p.dq[v].S);
+                uint32_t avail = (uint32_t)(sv >> 32) - (uint32_t)sv;
+                if (avail > Q) avail = 0;
+                // warp arg-max over (avail, lane)
+                uint32_t best = (avail << 5) | lane;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+                if ((best >> 5) == 0) { if (lane == 0) ++st_sfail; continue; }
+                const uint32_t bl = best & 31u;
+                const uint32_t victim = __shfl_sync(0xffffffffu, v, bl);
+                DequeMeta* vdq = p.dq + victim;
+                uint32_t got = 0, h0 = 0;
+                if (lane == 0) {
+                    if (atom_cas_relaxed(&vdq->lock, 0u, 1u) == 0u) {  // try-lock
+                        unsigned long long s = ld_relaxed(&vdq->S);
+                        for (int it = 0; it < 8; ++it) {
+                            const uint32_t h = (uint32_t)s, sp = (uint32_t)(s >> 32);
+                            const uint32_t a = sp - h;
+                            if (a == 0u || a > Q) break;
+                            const uint32_t c = min(p.steal_max, a);
+                            const unsigned long long nw = ((unsigned long long)sp << 32) | (uint32_t)(h + c);
+                            const unsigned long long o = atom_cas_acquire(&vdq->S, s, nw);
+                            if (o == s) { got = c; h0 = h; break; }
+                            s = o;
+                        }
+                        if (got == 0u) st_relaxed(&vdq->lock, 0u);
+                    }
+                }
+                got = __shfl_sync(0xffffffffu, got, 0);
+                h0 = __shfl_sync(0xffffffffu, h0, 0);
+                if (got) {
+                    // advance the read prefix only after loading the stolen IDs
+                    if (lane < got) my = ld_relaxed(&p.ring[(size_t)victim * Q + ((h0 + lane) & qmask)]);
+                    __syncwarp();
+                    if (lane == 0) {
+                        red_add_release(&vdq->steal_done, got);
+                        st_relaxed(&vdq->lock, 0u);
+                        ++st_sok;
+                        st_stolen += got;
+                    }
+                    n = got;
+                } else if (lane == 0) {
+                    ++st_sfail;
+                }
+            }
+        }
+        done_seen = __shfl_sync(0xffffffffu, done_seen, 0);
+        if (n == 0) {
+            // idle: termination check + watchdog + backoff
+            if (lane == 0) ++st_idle;
+            uint32_t d = 0;
+            if (lane == 0) d = ld_relaxed(&p.ctl->done);
+            d = __shfl_sync(0xffffffffu, d, 0);
+            if (d) break;
+            if (p.watchdog_ns && lane == 0 && globaltimer() - t0 > p.watchdog_ns) raise_error(p.ctl, GTAP_E_TIMEOUT);
+            nanosleep(backoff);
+            backoff = min(backoff * 2u, 2048u);
+            continue;
+        }
+        backoff = 32;
+        if (lane == 0) { ++st_cyc; st_inv += n; }
+
+        // ================= (2) execute, one task per lane =================
+        Out o;
+        o.init();
+        uint32_t parent = kNone, aux = 0, ord = 0, myfn = 0;
+        if (my != kNone) {
+            const uint4 h = ld_relaxed_v4(p.rec + my);
+            const uint4 dv = ld_relaxed_v4(&p.rec[my].d[0]);
+            const uint32_t d[kDataWords] = {dv.x, dv.y, dv.z, dv.w};
+            parent = h.z;
+            aux = h.w;
+            ord = meta_ord(h.x);
+            myfn = meta_fn(h.x);
+            T::exec(args, meta_fn(h.x), meta_state(h.x), d, o);
+            if (o.action == 0u) o.err = GTAP_E_BAD_STATE;
+        }
+        __syncwarp();
+        uint32_t err = o.err;
+
+        // ================= (3a) free + allocate =================
+        const bool fin = (o.action == Out::kFinish);
+        const uint32_t fball = __ballot_sync(0xffffffffu, fin);
+        const uint32_t F = __popc(fball);
+        if (fin) sm.fbuf[__popc(fball & lt)] = my;
+        uint32_t T_total;
+        const uint32_t nc = (err == 0u) ? o.nchild : 0u;
+        const uint32_t excl = warp_excl_scan(nc, lane, T_total);
+        const uint32_t fromF = min(F, T_total);
+        uint32_t need = T_total - fromF;
+        uint32_t fromRing = 0;
+        while (need > 0u) {  // drain the own free ring, 32 entries per round
+            const uint32_t want = min(need, 32u);
+            uint32_t e = 0;
+            if (lane < want) e = ld_relaxed(&myfring[(fhead + lane) & mmask]);
+            const uint32_t valid = __ballot_sync(0xffffffffu, e != 0u);
+            const uint32_t k = min((uint32_t)(__ffs(~valid) - 1), want);  // contiguous prefix
+            if (lane < k) {
+                sm.abuf[fromRing + lane] = e - 1u;
+                st_relaxed(&myfring[(fhead + lane) & mmask], 0u);
+            }
+            fhead += k;
+            fromRing += k;
+            need -= k;
+            if (k < want) break;
+        }
+        if (need > 0u) {
+            if (bump + need > M) {
+                if (lane == 0) raise_error(p.ctl, GTAP_E_POOL_EXHAUSTED);
+                failed = true;
+            } else {
+                for (uint32_t i = lane; i < need; i += 32) sm.abuf[fromRing + i] = base_id + bump + i;
+                bump += need;
+            }
+        }
+        __syncwarp();
+        if (failed) break;
+        if (lane == 0) st_tasks += T_total;
+
+        // ================= (3b) spawn: write child records =================
+        if (nc) {
+#pragma unroll
+            for (int c = 0; c < MAXC; ++c) {
+                if ((uint32_t)c < nc) {
+                    const uint32_t g = excl + c;
+                    const uint32_t cid = (g < fromF) ? sm.fbuf[g] : sm.abuf[g - fromF];
+                    TaskRec* cr = p.rec + cid;
+                    st_v4(cr, make_uint4(make_meta(o.cfn[c], 0, c, 0), 0u, T::kTaskwait ? my : kNone, 0u));
+                    st_v4(&cr->d[0], make_uint4(o.cd[c][0], o.cd[c][1], o.cd[c][2], o.cd[c][3]));
+                    sm.cbuf[g] = cid;
+                }
+            }
+        }
+        // suspend: store the resumption state and the join counter
+        uint32_t resume_id = kNone;
+        if (o.action == Out::kSuspend) {
+            st_v2(p.rec + my, make_meta(myfn, o.next_state, ord, 0), nc);
+            if (nc == 0u) resume_id = my;  // empty join: runnable at once
+        }
+        // surplus freed records go back to their home worker's free ring
+        if (F > T_total) {
+            const bool mine_free = lane < F - T_total;
+            const uint32_t mask = __ballot_sync(0xffffffffu, mine_free);
+            if (mine_free) {
+                const uint32_t id = sm.fbuf[T_total + lane];
+                const uint32_t home = id >> p.logM;
+                const uint32_t grp = __match_any_sync(mask, home);
+                const uint32_t leader = __ffs(grp) - 1u;
+                uint32_t base = 0;
+                if (lane == leader) base = atom_add_relaxed(&p.fm[home].tail, (uint32_t)__popc(grp));
+                base = __shfl_sync(grp, base, leader);
+                const uint32_t slot = base + __popc(grp & lt);
+                st_relaxed(&p.fring[((size_t)home << p.logM) + (slot & mmask)], id + 1u);
+            }
+            const uint32_t rf = __ballot_sync(0xffffffffu, mine_free && (sm.fbuf[T_total + lane] >> p.logM) != w);
+            if (lane == 0) st_rfree += __popc(rf);
+        }
+        // finish: copy the result into the parent's slot (copy-at-finish, R8)
+        if (fin && err == 0u && parent != kNone && o.has_result)
+            st_relaxed(reinterpret_cast<int32_t*>(&p.rec[parent].d[2 + ord]), o.result);
+        __syncwarp();
+
+        // ================= (3c) join: last child re-enqueues the parent =================
+        if (fin && err == 0u) {
+            if (parent != kNone) {
+                const int32_t old = atom_add_acq_rel(&p.rec[parent].pending, -1);
+                if (old == 1) resume_id = parent;
+            } else if (aux & kRootFlag) {
+                const uint32_t r = aux & ~kRootFlag;
+                p.root_results[r] = o.has_result ? (long long)o.result : 0ll;
+                if (T::kTaskwait) {
+                    if (atom_add_acq_rel(&p.ctl->roots_left, 0xFFFFFFFFu) == 1u) st_release(&p.ctl->done, 1u);
+                }
+            }
+        }
+        {
+            const uint32_t eb = __ballot_sync(0xffffffffu, err != 0u);
+            if (eb && lane == (uint32_t)__ffs(eb) - 1u) raise_error(p.ctl, err);
+        }
+        if (!T::kTaskwait) {
+            // outstanding-task counter (SPEC S:321 reading): +children -finished, one atomic per warp-cycle
+            const long long delta = (long long)T_total - (long long)F;
+            if (lane == 0 && delta != 0) {
+                const long long old = atom_add_acq_rel(&p.ctl->outstanding, delta);
+                if (old + delta == 0) st_release(&p.ctl->done, 1u);
+            }
+        }
+
+        // ================= (3d) distribute: keep <= 32, push the rest =================
+        const uint32_t rball = __ballot_sync(0xffffffffu, resume_id != kNone);
+        const uint32_t P = __popc(rball);
+        if (resume_id != kNone) sm.pbuf[__popc(rball & lt)] = resume_id;
+        __syncwarp();
+        const uint32_t R = P + T_total;
+        const uint32_t keep = min(R, 32u);
+        uint32_t pushc = R - keep;
+        if (pushc) {
+            if (tail + pushc - sdone > Q) {
+                if (lane == 0) sdone = ld_relaxed(&mydq->steal_done);
+                sdone = __shfl_sync(0xffffffffu, sdone, 0);
+                if (tail + pushc - sdone > Q) {
+                    if (lane == 0) raise_error(p.ctl, GTAP_E_QUEUE_OVERFLOW);
+                    break;
+                }
+            }
+        }
+        for (uint32_t i = lane; i < R; i += 32) {
+            const uint32_t id = (i < P) ? sm.pbuf[i] : sm.cbuf[i - P];
+            if (i < keep) sm.kept[i] = id;
+            else ring[(tail + (i - keep)) & qmask] = id;
+        }
+        tail += pushc;
+        nkept = keep;
+        if (lane == 0) st_push += pushc;
+        // publish the oldest half of the private part when thieves drained the public part
+        if (lane == 0) {
+            const uint32_t h = (uint32_t)S_seen;
+            const uint32_t priv = tail - split;
+            if (h == split && priv >= 2u) {
+                const uint32_t k = priv >> 1;
+                split += k;
+                red_add_release(&mydq->S, (unsigned long long)k << 32);
+            }
+        }
+        split = __shfl_sync(0xffffffffu, split, 0);
+        __syncwarp();
+        if (done_seen) break;  // error raised elsewhere (completion implies no tasks left)
+        if (p.watchdog_ns && ((++cyc_u) & 4095u) == 0u) {
+            uint32_t tmo = 0;
+            if (lane == 0 && globaltimer() - t0 > p.watchdog_ns) { raise_error(p.ctl, GTAP_E_TIMEOUT); tmo = 1; }
+            if (__shfl_sync(0xffffffffu, tmo, 0)) break;
+        }
+    }
+
+    // ---- exit: fold per-warp counters into the control block
+    if (lane == 0) {
+        unsigned long long* s = p.ctl->stats;
+        atomicAdd(&s[ST_TASKS], st_tasks);
+        atomicAdd(&s[ST_INVOC], st_inv);
+        atomicAdd(&s[ST_POPS], st_pops);
+        atomicAdd(&s[ST_KEPT], st_kept);
+        atomicAdd(&s[ST_STEALS_OK], st_sok);
+        atomicAdd(&s[ST_STEALS_FAILED], st_sfail);
+        atomicAdd(&s[ST_STOLEN], st_stolen);
+        atomicAdd(&s[ST_PUSHES], st_push);
+        atomicAdd(&s[ST_CYCLES], st_cyc);
+        atomicAdd(&s[ST_IDLE], st_idle);
+        atomicAdd(&s[ST_REMOTE_FREES], st_rfree);
+        atomicMax(&s[ST_MAX_POOL], (unsigned long long)bump);
+    }
+}
+
+}  // namespace gtap

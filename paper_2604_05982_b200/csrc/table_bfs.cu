@@ -1,0 +1,95 @@
+// table_bfs.cu -- BFS frontier-expansion task table (block-level, no taskwait).
+//
+// PAPER.md P:1053-1068 (Prog. parallel graph traversal):
+//   bfs(v): dv = g_depth[v];
+//           for (e = row_start + threadIdx.x; e < row_end; e += blockDim.x) {
+//             u = g_col_indices[e]; old = atomicMin(&g_depth[u], dv + 1);
+//             if (old > dv + 1) spawn bfs(u);
+//           }
+// dv is read with an L1-bypassing load (depth is shared mutable
+// state written by other SMs). The edge loop runs in chunks of blockDim with
+// a uniform flush point every kChunk chunks, so a hub vertex cannot overflow
+// the shared-memory spawn staging (kSpawnCap). Payload: d[0] = v.
+#include "table_common.cuh"
+
+namespace gtap {
+
+struct BfsTable {
+    static constexpr uint32_t kKind = GTAP_WORKER_BLOCK;
+    static constexpr int kMaxChildren = 0;  // dynamic (no taskwait: no join metadata)
+    static constexpr bool kTaskwait = false;
+    static constexpr uint32_t kNumFn = 1;
+    static constexpr int kSpawnCap = 1536;
+    struct Scratch {
+        uint32_t unused;
+    };
+    struct Args {
+        const int32_t* row_ptr;
+        const int32_t* col;
+        int32_t* depth;
+        uint32_t nv;
+        uint32_t pad;
+    };
+    template <class Ctx>
+    __device__ __forceinline__ static void exec_block(const Args& a, Ctx& ctx, uint32_t fn, uint32_t state,
+                                                      const uint32_t (&d)[kDataWords]) {
+        if (fn != 0u || state != 0u) {
+            if (threadIdx.x == 0) ctx.bad_state();
+            return;
+        }
+        const uint32_t v = d[0];
+        const int32_t dv = dev::ld_relaxed(&a.depth[v]);
+        const int32_t s = __ldg(&a.row_ptr[v]), e = __ldg(&a.row_ptr[v + 1]);
+        const int32_t nd = dv + 1;
+        const uint32_t bd = blockDim.x;
+        const uint32_t chunk_every = max(1u, (uint32_t)kSpawnCap / (2u * bd));  // spawns between checks <= chunk_every*bd
+        uint32_t k = 0;
+        for (int32_t base = s; base < e; base += (int32_t)bd) {
+            const int32_t i = base + (int32_t)threadIdx.x;
+            if (i < e) {
+                const int32_t u = __ldg(&a.col[i]);
+                const int32_t old = atomicMin(&a.depth[u], nd);
+                if (old > nd) ctx.spawn(0u, (uint32_t)u);
+            }
+            if (++k == chunk_every) {                               // uniform
+                k = 0;
+                if (base + (int32_t)bd < e) ctx.flush(chunk_every * bd);
+            }
+        }
+        if (threadIdx.x == 0) ctx.finish_void();
+    }
+};
+
+static int validate_bfs(const gtap_task_table* t, uint32_t fn, const uint32_t* d) {
+    BfsTable::Args a;
+    std::memcpy(&a, t->args, sizeof(a));
+    return (fn == 0u && d[0] < a.nv) ? 0 : -1;
+}
+
+}  // namespace gtap
+
+extern "C" const gtap_task_table* gtap_table_bfs(const int32_t* row_ptr, const int32_t* col, int32_t* depth,
+                                                 uint32_t nv) {
+    if (!row_ptr || !col || !depth || nv == 0) return nullptr;
+    gtap::BfsTable::Args a{row_ptr, col, depth, nv, 0u};
+    return gtap::make_table<gtap::BfsTable>("bfs", a, &gtap::validate_bfs);
+}
+
+namespace {
+__global__ void bfs_init_depth_kernel(int32_t* __restrict__ depth, uint32_t nv, int32_t src) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t v = i; v < nv; v += stride) depth[v] = (v == (uint32_t)src) ? 0 : 0x7fffffff;
+}
+}  // namespace
+
+// depth[v] = INT32_MAX for v != src, depth[src] = 0 (reading R18), on `stream`.
+extern "C" gtap_status gtap_bfs_init_depth(int32_t* depth, uint32_t nv, int32_t src, void* stream) {
+    if (!depth || nv == 0 || src < 0 || (uint32_t)src >= nv) return GTAP_E_INVAL;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const uint32_t blocks = min((nv + 255u) / 256u, (uint32_t)sms * 8u);
+    bfs_init_depth_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(depth, nv, src);
+    return cudaGetLastError() == cudaSuccess ? GTAP_OK : GTAP_E_CUDA;
+}

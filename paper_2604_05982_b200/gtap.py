@@ -1,0 +1,302 @@
+"""ctypes binding of the C ABI in include/gtap.h (argument marshalling only).
+
+Every step of the hot path runs in libgtap.so's CUDA kernels; this module
+converts Python/torch arguments to plain pointers and sizes, allocates the
+runtime workspace through PyTorch (caller-owned device memory) and turns
+status codes into exceptions. It never computes task results itself and has
+no CPU fallback: if libgtap.so is missing or no B200 is present, it raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libgtap.so")
+
+GTAP_WORKER_THREAD = 0
+GTAP_WORKER_BLOCK = 1
+
+STATUS = {
+    0: "GTAP_OK", 1: "GTAP_E_INVAL", 2: "GTAP_E_CUDA", 3: "GTAP_E_NOMEM", 4: "GTAP_E_BUSY",
+    5: "GTAP_E_POOL_EXHAUSTED", 6: "GTAP_E_QUEUE_OVERFLOW", 7: "GTAP_E_CHILD_LIMIT",
+    8: "GTAP_E_TIMEOUT", 9: "GTAP_E_BAD_STATE", 10: "GTAP_E_NO_DEVICE", 11: "GTAP_E_UNSUPPORTED",
+}
+
+
+class GtapError(RuntimeError):
+    def __init__(self, code: int, where: str):
+        self.code = code
+        super().__init__(f"{where}: {STATUS.get(code, code)}")
+
+
+class Config(ctypes.Structure):
+    _fields_ = [
+        ("struct_size", ctypes.c_uint32), ("device", ctypes.c_int32), ("worker_kind", ctypes.c_uint32),
+        ("grid_size", ctypes.c_uint32), ("block_size", ctypes.c_uint32),
+        ("max_tasks_per_worker", ctypes.c_uint32), ("queue_capacity", ctypes.c_uint32),
+        ("max_child_tasks", ctypes.c_uint32), ("num_queues", ctypes.c_uint32),
+        ("max_task_data_size", ctypes.c_uint32), ("assume_no_taskwait", ctypes.c_uint32),
+        ("steal_attempts", ctypes.c_uint32), ("steal_max", ctypes.c_uint32), ("max_roots", ctypes.c_uint32),
+        ("seed", ctypes.c_uint64), ("watchdog_ns", ctypes.c_uint64),
+    ]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [
+        ("tasks", ctypes.c_uint64), ("invocations", ctypes.c_uint64), ("pops", ctypes.c_uint64),
+        ("kept", ctypes.c_uint64), ("steals_ok", ctypes.c_uint64), ("steals_failed", ctypes.c_uint64),
+        ("stolen_tasks", ctypes.c_uint64), ("pushes", ctypes.c_uint64), ("cycles", ctypes.c_uint64),
+        ("idle_cycles", ctypes.c_uint64), ("remote_frees", ctypes.c_uint64), ("max_pool_used", ctypes.c_uint64),
+        ("error_word", ctypes.c_uint32), ("workers", ctypes.c_uint32), ("device_ms", ctypes.c_float),
+        ("grid_size", ctypes.c_uint32), ("block_size", ctypes.c_uint32), ("reserved", ctypes.c_uint32 * 2),
+    ]
+
+    def as_dict(self) -> dict:
+        return {k: (getattr(self, k) if k != "reserved" else None) for k, _ in self._fields_ if k != "reserved"}
+
+
+# Every symbol include/gtap.h declares (checked by tests/test_abi.py).
+EXPORTS = [
+    "gtap_abi_version", "gtap_status_str", "gtap_config_default", "gtap_workspace_bytes", "gtap_init",
+    "gtap_spawn_root", "gtap_reset", "gtap_run", "gtap_sync", "gtap_root_result", "gtap_finalize",
+    "gtap_geometry", "gtap_table_destroy", "gtap_table_fib", "gtap_table_mergesort", "gtap_table_spmv",
+    "gtap_table_bfs", "gtap_bfs_init_depth", "gtap_ubench_atomics",
+]
+
+_lib = None
+
+
+def lib():
+    """Load libgtap.so (raises if it was not built: there is no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} missing: run python -c 'import __graft_entry__ as g; g.build()'")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, u32, i32, u64, sz = ctypes.c_void_p, ctypes.c_uint32, ctypes.c_int32, ctypes.c_uint64, ctypes.c_size_t
+    P = ctypes.POINTER
+    L.gtap_abi_version.restype = u32
+    L.gtap_status_str.restype = ctypes.c_char_p
+    L.gtap_status_str.argtypes = [ctypes.c_int]
+    L.gtap_config_default.argtypes = [P(Config), i32, u32]
+    L.gtap_workspace_bytes.argtypes = [P(Config)]
+    L.gtap_workspace_bytes.restype = sz
+    L.gtap_init.argtypes = [P(Config), vp, sz, P(vp)]
+    L.gtap_spawn_root.argtypes = [vp, vp, u32, vp, u32, P(u32)]
+    L.gtap_reset.argtypes = [vp, vp]
+    L.gtap_run.argtypes = [vp, vp]
+    L.gtap_sync.argtypes = [vp, P(Stats)]
+    L.gtap_root_result.argtypes = [vp, u32, vp, u32]
+    L.gtap_finalize.argtypes = [vp]
+    L.gtap_geometry.argtypes = [vp, vp, P(u32), P(u32), P(u32)]
+    L.gtap_table_destroy.argtypes = [vp]
+    L.gtap_table_destroy.restype = None
+    L.gtap_table_fib.argtypes = []
+    L.gtap_table_fib.restype = vp
+    L.gtap_table_mergesort.argtypes = [vp, vp, u64, i32]
+    L.gtap_table_mergesort.restype = vp
+    L.gtap_table_spmv.argtypes = [vp, vp, vp, vp, vp, u32, u32, u32]
+    L.gtap_table_spmv.restype = vp
+    L.gtap_table_bfs.argtypes = [vp, vp, vp, u32]
+    L.gtap_table_bfs.restype = vp
+    L.gtap_bfs_init_depth.argtypes = [vp, u32, i32, vp]
+    L.gtap_ubench_atomics.argtypes = [vp, u64, u32, u32, u32, u32, vp, P(ctypes.c_float)]
+    for name in ("gtap_config_default", "gtap_init", "gtap_spawn_root", "gtap_reset", "gtap_run", "gtap_sync",
+                 "gtap_root_result", "gtap_finalize", "gtap_geometry", "gtap_ubench_atomics", "gtap_bfs_init_depth"):
+        getattr(L, name).restype = ctypes.c_int
+    _lib = L
+    return L
+
+
+def _check(code: int, where: str):
+    if code != 0:
+        raise GtapError(code, where)
+
+
+def _stream_ptr(stream) -> int | None:
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream or None
+    return getattr(stream, "cuda_stream", stream) or None
+
+
+class Table:
+    """A task table (one persistent-kernel instantiation + its constant args).
+
+    Holds references to the tensors whose pointers the table captured so they
+    outlive every run that uses it."""
+
+    def __init__(self, ptr: int, name: str, kind: int, keep=()):
+        if not ptr:
+            raise GtapError(1, f"gtap_table_{name}")
+        self.ptr = ptr
+        self.name = name
+        self.kind = kind
+        self._keep = tuple(keep)
+
+    def close(self):
+        if self.ptr:
+            lib().gtap_table_destroy(self.ptr)
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- constructors (include/gtap.h) ----
+    @staticmethod
+    def fib() -> "Table":
+        return Table(lib().gtap_table_fib(), "fib", GTAP_WORKER_THREAD)
+
+    @staticmethod
+    def mergesort(keys, scratch, cutoff: int = 128) -> "Table":
+        _dev_i32(keys, "keys"); _dev_i32(scratch, "scratch")
+        if scratch.numel() < keys.numel():
+            raise ValueError("scratch must hold n keys")
+        return Table(lib().gtap_table_mergesort(keys.data_ptr(), scratch.data_ptr(), keys.numel(), cutoff),
+                     "mergesort", GTAP_WORKER_THREAD, (keys, scratch))
+
+    @staticmethod
+    def spmv(row_ptr, col, val, x, y, nnz_cut: int = 8192, fanout: int = 16) -> "Table":
+        for t, n in ((row_ptr, "row_ptr"), (col, "col")):
+            _dev_i32(t, n)
+        nrows = row_ptr.numel() - 1
+        return Table(lib().gtap_table_spmv(row_ptr.data_ptr(), col.data_ptr(), val.data_ptr(), x.data_ptr(),
+                                           y.data_ptr(), nrows, nnz_cut, fanout),
+                     "spmv", GTAP_WORKER_BLOCK, (row_ptr, col, val, x, y))
+
+    @staticmethod
+    def bfs(row_ptr, col, depth) -> "Table":
+        _dev_i32(row_ptr, "row_ptr"); _dev_i32(col, "col"); _dev_i32(depth, "depth")
+        return Table(lib().gtap_table_bfs(row_ptr.data_ptr(), col.data_ptr(), depth.data_ptr(), depth.numel()),
+                     "bfs", GTAP_WORKER_BLOCK, (row_ptr, col, depth))
+
+
+def _dev_i32(t, name):
+    import torch
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.int32 and t.is_contiguous()):
+        raise TypeError(f"{name} must be a contiguous CUDA int32 tensor")
+
+
+@dataclass
+class RunStats:
+    tasks: int
+    invocations: int
+    pops: int
+    kept: int
+    steals_ok: int
+    steals_failed: int
+    stolen_tasks: int
+    pushes: int
+    cycles: int
+    idle_cycles: int
+    remote_frees: int
+    max_pool_used: int
+    error_word: int
+    workers: int
+    device_ms: float
+    grid_size: int
+    block_size: int
+
+
+class Runtime:
+    """gtap_init / gtap_finalize around a torch-allocated workspace."""
+
+    def __init__(self, kind: int, device: int = 0, *, grid_size: int = 0, block_size: int = 0,
+                 max_tasks_per_worker: int = 0, queue_capacity: int = 0, steal_attempts: int = 0,
+                 steal_max: int = 0, seed: int = 0x5EED, watchdog_ns: int = 0, max_roots: int = 0,
+                 torch_workspace: bool = True):
+        import torch
+        L = lib()
+        cfg = Config()
+        _check(L.gtap_config_default(ctypes.byref(cfg), device, kind), "gtap_config_default")
+        for k, v in dict(grid_size=grid_size, block_size=block_size, max_tasks_per_worker=max_tasks_per_worker,
+                         queue_capacity=queue_capacity, steal_attempts=steal_attempts, steal_max=steal_max,
+                         watchdog_ns=watchdog_ns, max_roots=max_roots).items():
+            if v:
+                setattr(cfg, k, v)
+        cfg.seed = seed
+        self.cfg = cfg
+        self.kind = kind
+        self.device = device
+        nbytes = L.gtap_workspace_bytes(ctypes.byref(cfg))
+        if nbytes == 0:
+            raise GtapError(1, "gtap_workspace_bytes")
+        self.workspace = None
+        ptr = None
+        if torch_workspace:
+            self.workspace = torch.empty(nbytes + 256, dtype=torch.uint8, device=f"cuda:{device}")
+            ptr = (self.workspace.data_ptr() + 255) // 256 * 256
+        h = ctypes.c_void_p()
+        _check(L.gtap_init(ctypes.byref(cfg), ptr, nbytes, ctypes.byref(h)), "gtap_init")
+        self.h = h.value
+        self.workspace_bytes = nbytes
+
+    def spawn_root(self, table: Table, args=(), fn: int = 0) -> int:
+        words = (ctypes.c_uint32 * 4)(*[int(a) & 0xFFFFFFFF for a in args])
+        idx = ctypes.c_uint32()
+        _check(lib().gtap_spawn_root(self.h, table.ptr, fn, words, 4 * len(args), ctypes.byref(idx)),
+               "gtap_spawn_root")
+        return idx.value
+
+    def run(self, stream=None):
+        _check(lib().gtap_run(self.h, _stream_ptr(stream)), "gtap_run")
+
+    def sync(self, raise_on_error: bool = True) -> RunStats:
+        st = Stats()
+        code = lib().gtap_sync(self.h, ctypes.byref(st))
+        if raise_on_error:
+            _check(code, "gtap_sync")
+        d = st.as_dict()
+        return RunStats(**d)
+
+    def reset(self, stream=None):
+        _check(lib().gtap_reset(self.h, _stream_ptr(stream)), "gtap_reset")
+
+    def root_result(self, idx: int = 0) -> int:
+        v = ctypes.c_int64()
+        _check(lib().gtap_root_result(self.h, idx, ctypes.byref(v), 8), "gtap_root_result")
+        return v.value
+
+    def geometry(self, table: Table):
+        W, g, b = ctypes.c_uint32(), ctypes.c_uint32(), ctypes.c_uint32()
+        _check(lib().gtap_geometry(self.h, table.ptr, ctypes.byref(W), ctypes.byref(g), ctypes.byref(b)),
+               "gtap_geometry")
+        return W.value, g.value, b.value
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().gtap_finalize(self.h)
+            self.h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def ubench_atomics(buf, kind: int, grid: int, block: int, ops_per_thread: int, stream=None) -> float:
+    """Kernel ms of the L2-atomic probe `kind` (see gtap.h) over the int32 CUDA tensor buf."""
+    ms = ctypes.c_float()
+    _check(lib().gtap_ubench_atomics(buf.data_ptr(), buf.numel(), kind, grid, block, ops_per_thread,
+                                     _stream_ptr(stream), ctypes.byref(ms)), "gtap_ubench_atomics")
+    return ms.value
+
+
+def bfs_init_depth(depth, src: int, stream=None):
+    """depth[:] = INT32_MAX, depth[src] = 0 on the device (libgtap kernel)."""
+    _dev_i32(depth, "depth")
+    _check(lib().gtap_bfs_init_depth(depth.data_ptr(), depth.numel(), src, _stream_ptr(stream)),
+           "gtap_bfs_init_depth")

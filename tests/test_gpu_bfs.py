@@ -1,0 +1,107 @@
+"""GPU parity: BFS task table vs FIFO BFS (bit-exact levels).
+
+PAPER.md P:1053-1068. Small special graphs, random small graphs, RMAT graphs
+from several sources, and BASELINE configs[4] (RMAT scale 22, edge factor 16)
+at the bench's launch configuration. The task count is nondeterministic
+(reading in DESIGN.md: parity unpinned), so only its lower bound is checked.
+"""
+import itertools
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+WD = 30_000_000_000
+
+
+@pytest.fixture(scope="module")
+def g(cuda_device):
+    import paper_2604_05982_b200 as g
+    return g
+
+
+@pytest.fixture(scope="module")
+def rt(g):
+    r = g.Runtime(g.GTAP_WORKER_BLOCK, 0, grid_size=148 * 2, block_size=128, max_tasks_per_worker=4096,
+                  watchdog_ns=WD)
+    yield r
+    r.close()
+
+
+def csr_from_edges(nv, edges):
+    adj = [[] for _ in range(nv)]
+    for u, v in edges:
+        adj[u].append(v)
+        adj[v].append(u)
+    rp = [0]
+    col = []
+    for a in adj:
+        col += sorted(a)
+        rp.append(len(col))
+    return torch.tensor(rp, dtype=torch.int32), torch.tensor(col if col else [0], dtype=torch.int32)
+
+
+def check(g, rt, rp, col, src):
+    depth, st = g.bfs(rp.cuda(), col.cuda(), src, rt=rt)
+    ref = oracle.bfs(rp, col[: int(rp[-1])] if int(rp[-1]) else col, src)
+    assert np.array_equal(depth.cpu().numpy(), ref)
+    reached = int((ref != oracle.INT32_MAX).sum())
+    assert st.tasks >= reached  # every reached vertex was expanded at least once
+    return st
+
+
+def test_special_graphs(g, rt):
+    n = 300
+    check(g, rt, *csr_from_edges(n, [(i, i + 1) for i in range(n - 1)]), 0)        # path
+    check(g, rt, *csr_from_edges(n, [(0, i) for i in range(1, n)]), 5)            # star from a leaf
+    check(g, rt, *csr_from_edges(60, list(itertools.combinations(range(60), 2))), 7)  # complete
+    check(g, rt, *csr_from_edges(50, [(1, 2), (3, 4)]), 0)                         # isolated source
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_random_small(g, rt, seed):
+    rng = np.random.default_rng(seed)
+    nv = int(rng.integers(2, 200))
+    m = int(rng.integers(0, 4 * nv))
+    edges = [tuple(rng.integers(0, nv, 2).tolist()) for _ in range(m)]
+    rp, col = csr_from_edges(nv, edges)
+    check(g, rt, rp, col, int(rng.integers(0, nv)))
+
+
+@pytest.mark.parametrize("scale", [10, 14, 16])
+def test_rmat(g, rt, scale):
+    rp, col = synth.rmat_csr(scale, 16, seed=scale)
+    for s in synth.bfs_sources(rp, 3, seed=scale):
+        check(g, rt, rp, col, s)
+
+
+def test_hub_overflows_staging(g):
+    # one vertex adjacent to 20k others: spawns exceed the shared-memory staging and are flushed mid-task
+    n = 20001
+    with g.Runtime(g.GTAP_WORKER_BLOCK, 0, grid_size=148, block_size=256, max_tasks_per_worker=1 << 15,
+                   watchdog_ns=WD) as r:
+        check(g, r, *csr_from_edges(n, [(0, i) for i in range(1, n)]), 0)
+
+
+def test_hub_capacity_error(g):
+    # the same hub with a 4096-slot deque must fail loudly (fixed capacity), not hang
+    n = 20001
+    with g.Runtime(g.GTAP_WORKER_BLOCK, 0, grid_size=16, block_size=256, max_tasks_per_worker=4096,
+                   watchdog_ns=WD) as r:
+        with pytest.raises(g.GtapError) as e:
+            check(g, r, *csr_from_edges(n, [(0, i) for i in range(1, n)]), 0)
+        assert e.value.code in (5, 6)
+
+
+def test_full_size_config4(g):
+    import bench
+    rp, col = synth.rmat_csr(22, 16, seed=3, device="cuda")
+    src = synth.bfs_sources(rp, 1, seed=5)[0]
+    with g.Runtime(g.GTAP_WORKER_BLOCK, 0, watchdog_ns=60_000_000_000, **bench.BFS_CFG) as r:
+        depth, st = g.bfs(rp, col, src, rt=r)
+    ref = oracle.bfs(rp.cpu(), col.cpu(), src)
+    assert np.array_equal(depth.cpu().numpy(), ref)

@@ -1,0 +1,98 @@
+"""GPU parity: mergesort task table vs the oracle (bit-exact output, exact task counts).
+
+PAPER.md P:59-74. Ragged sizes around the cutoff and the
+32-lane tile, every cutoff the API allows at its edges, adversarial inputs,
+forests, and BASELINE configs[1] (2^24 random int32) at the bench's launch
+configuration.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+WD = 30_000_000_000
+
+
+@pytest.fixture(scope="module")
+def g(cuda_device):
+    import paper_2604_05982_b200 as g
+    return g
+
+
+@pytest.fixture(scope="module")
+def rt(g):
+    r = g.Runtime(g.GTAP_WORKER_THREAD, 0, grid_size=148 * 2, block_size=128, max_tasks_per_worker=1024,
+                  watchdog_ns=WD)
+    yield r
+    r.close()
+
+
+def run_sort(g, rt, keys_np, cutoff=128):
+    import torch
+    d = torch.from_numpy(keys_np).cuda()
+    st = g.mergesort_(d, cutoff=cutoff, rt=rt)
+    return d.cpu().numpy(), st
+
+
+@pytest.mark.parametrize("n", [0, 1, 2, 31, 127, 128, 129, 255, 256, 1000, 4097, (1 << 16) + 7, 1 << 20])
+def test_sizes(g, rt, n):
+    keys = synth.keys_int32(n, seed=n).numpy()
+    out, st = run_sort(g, rt, keys)
+    ref, tasks, inv = oracle.mergesort(keys, 128)
+    assert np.array_equal(out, ref)
+    assert (st.tasks, st.invocations) == (tasks, inv)
+
+
+@pytest.mark.parametrize("cutoff", [1, 2, 3, 64, 128, 255, 256])
+def test_cutoffs(g, rt, cutoff):
+    keys = synth.keys_int32(20011, seed=cutoff).numpy()
+    out, st = run_sort(g, rt, keys, cutoff)
+    ref, tasks, inv = oracle.mergesort(keys, cutoff)
+    assert np.array_equal(out, ref)
+    assert (st.tasks, st.invocations) == (tasks, inv)
+
+
+@pytest.mark.parametrize("kind", ["sorted", "reverse", "equal", "two", "extremes"])
+def test_adversarial(g, rt, kind):
+    n = 100003
+    rng = np.random.default_rng(7)
+    a = {"sorted": np.arange(n), "reverse": np.arange(n, 0, -1), "equal": np.full(n, 3),
+         "two": rng.integers(0, 2, n),
+         "extremes": rng.choice(np.array([-2**31, 2**31 - 1, 0, -1]), n)}[kind].astype(np.int32)
+    out, _ = run_sort(g, rt, a)
+    assert np.array_equal(out, oracle.mergesort(a, 128)[0])
+
+
+def test_forest(g):
+    import torch
+    seg = 1 << 14
+    k = 37
+    keys = synth.keys_int32(seg * k + 5, seed=3).numpy()
+    segments = [(i * seg, (i + 1) * seg) for i in range(k)] + [(seg * k, seg * k + 5)]
+    d = torch.from_numpy(keys).cuda()
+    st = g.mergesort_forest_(d, segments, grid_size=148, block_size=128, max_tasks_per_worker=1024,
+                             watchdog_ns=WD)
+    out = d.cpu().numpy()
+    tasks = 0
+    for l, r in segments:
+        ref, t, _ = oracle.mergesort(keys[l:r], 128)
+        assert np.array_equal(out[l:r], ref)
+        tasks += t
+    assert st.tasks == tasks
+
+
+def test_full_size_config1(g):
+    """BASELINE configs[1]: 2^24 random int32 keys, cutoff 128, the bench's launch configuration."""
+    import torch
+
+    import bench
+    n = 1 << 24
+    keys = synth.keys_int32(n, seed=42)
+    d = keys.cuda()
+    with g.Runtime(g.GTAP_WORKER_THREAD, 0, watchdog_ns=60_000_000_000, **bench.MS_CFG) as r:
+        st = g.mergesort_(d, cutoff=128, rt=r)
+    ref, tasks, inv = oracle.mergesort(keys.numpy(), 128)
+    assert np.array_equal(d.cpu().numpy(), ref)
+    assert (st.tasks, st.invocations) == (tasks, inv) == (262143, 393214)

@@ -183,7 +183,7 @@ __device__ __forceinline__ void block_maybe_publish(const KParams& p, BLeader& L
 }
 
 template <class T>
-__global__ void __launch_bounds__(1024) block_sched_kernel(KParams p, typename T::Args args) {
+__global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) block_sched_kernel(KParams p, typename T::Args args) {
     using namespace dev;
     __shared__ BlockSmem<T> sm;
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;

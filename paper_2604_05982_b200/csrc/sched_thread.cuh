@@ -67,7 +67,7 @@ struct WarpSmem {
 };
 
 template <class T>
-__global__ void __launch_bounds__(1024) thread_sched_kernel(KParams p, typename T::Args args) {
+__global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_kernel(KParams p, typename T::Args args) {
     using namespace dev;
     constexpr int MAXC = T::kMaxChildren;
     using Out = TOut<MAXC>;

@@ -16,6 +16,7 @@ struct FibTable {
     static constexpr int kMaxChildren = 2;
     static constexpr bool kTaskwait = true;
     static constexpr uint32_t kNumFn = 1;
+    static constexpr int kMaxThreads = 256, kMinBlocks = 4;  // __launch_bounds__
     struct Args {
         uint32_t unused;
     };

@@ -21,11 +21,76 @@ namespace gtap {
 
 constexpr int kMsMaxCutoff = 256;
 
+
+// One thread merges src[l, m) and src[m, r) into dst[l, r) (thread-executed
+// task; the paper's merge is "largely sequential and executed by a
+// single thread-level worker"). Two independent dependency chains run
+// interleaved: the front chain emits the ceil(n/2) smallest keys (ties: left
+// run first), the back chain the floor(n/2) largest (ties: right run last), so
+// the output equals the plain two-pointer stable merge. In long stretches
+// where no run can end, each chain reads its runs through 4-key register
+// windows refilled 4 keys ahead (no bounds checks, no sentinels) with L1
+// prefetches 512 B further out; near the run ends a checked scalar step is used.
+__device__ __noinline__ void ms_merge(const int32_t* __restrict__ src, int32_t* __restrict__ dst, uint32_t l,
+                                      uint32_t m, uint32_t r) {
+    const uint32_t n = r - l;
+    const uint32_t nf = (n + 1u) >> 1, nb = n - nf;
+    uint32_t ia = l, ib = m, kf = l;          // front chain
+    int32_t ja = (int32_t)m - 1, jb = (int32_t)r - 1;  // back chain (inclusive tails)
+    uint32_t kb = r - 1u;
+    uint32_t done = 0;                         // paired steps done (front and back each)
+    while (done < nb) {
+        // unchecked steps available: every window refill index stays inside its run
+        int64_t S = (int64_t)min(min(m - ia, r - ib), min((uint32_t)(ja - (int32_t)l + 1), (uint32_t)(jb - (int32_t)m + 1))) - 5;
+        S = min(S, (int64_t)(nb - done));
+        if (S >= 16) {
+            int32_t a0 = src[ia], a1 = src[ia + 1], a2 = src[ia + 2], a3 = src[ia + 3];
+            int32_t b0 = src[ib], b1 = src[ib + 1], b2 = src[ib + 2], b3 = src[ib + 3];
+            int32_t c0 = src[ja], c1 = src[ja - 1], c2 = src[ja - 2], c3 = src[ja - 3];
+            int32_t e0 = src[jb], e1 = src[jb - 1], e2 = src[jb - 2], e3 = src[jb - 3];
+            const uint32_t steps = (uint32_t)S;
+            for (uint32_t t = 0; t < steps; ++t) {
+                if ((t & 7u) == 0u) {
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(src + min(ia + 128u, m - 1u)));
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(src + min(ib + 128u, r - 1u)));
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(src + max(ja - 128, (int32_t)l)));
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(src + max(jb - 128, (int32_t)m)));
+                }
+                if (b0 < a0) {  // front: right run only if strictly smaller
+                    dst[kf] = b0; b0 = b1; b1 = b2; b2 = b3; b3 = src[ib + 4]; ++ib;
+                } else {
+                    dst[kf] = a0; a0 = a1; a1 = a2; a2 = a3; a3 = src[ia + 4]; ++ia;
+                }
+                ++kf;
+                if (c0 > e0) {  // back: left run only if strictly larger
+                    dst[kb] = c0; c0 = c1; c1 = c2; c2 = c3; c3 = src[ja - 4]; --ja;
+                } else {
+                    dst[kb] = e0; e0 = e1; e1 = e2; e2 = e3; e3 = src[jb - 4]; --jb;
+                }
+                --kb;
+            }
+            done += steps;
+        } else {
+            // checked scalar step for each chain
+            const bool takeB = ib < r && (ia >= m || src[ib] < src[ia]);
+            dst[kf++] = takeB ? src[ib++] : src[ia++];
+            const bool takeA = ja >= (int32_t)l && (jb < (int32_t)m || src[ja] > src[jb]);
+            dst[kb--] = takeA ? src[ja--] : src[jb--];
+            ++done;
+        }
+    }
+    if (nf > nb) {
+        const bool takeB = ib < r && (ia >= m || src[ib] < src[ia]);
+        dst[kf] = takeB ? src[ib] : src[ia];
+    }
+}
+
 struct MergesortTable {
     static constexpr uint32_t kKind = GTAP_WORKER_THREAD;
     static constexpr int kMaxChildren = 2;
     static constexpr bool kTaskwait = true;
     static constexpr uint32_t kNumFn = 1;
+    static constexpr int kMaxThreads = 128, kMinBlocks = 4;  // __launch_bounds__: 128 regs, no spills
     struct Args {
         int32_t* keys;
         int32_t* scratch;
@@ -55,64 +120,9 @@ struct MergesortTable {
     }
 
     // merge: stable merge of src[l, m) and src[m, r) into dst[l, r).
-    // One thread, two independent chains: the front chain emits the
-    // ceil(n/2) smallest keys (ties -> left run first), the back chain the
-    // floor(n/2) largest (ties -> right run first), so the result equals the
-    // plain two-pointer merge. Each run is read through a 4-key register
-    // window refilled one key ahead, with L1 prefetches 128 B further out,
-    // so the dependent chain is compare + select rather than load latency.
-    __device__ __noinline__ static void merge(const int32_t* __restrict__ src, int32_t* __restrict__ dst, uint32_t l,
-                                              uint32_t m, uint32_t r) {
-        const long long PINF = 0x7fffffffffffffffll, NINF = (long long)0x8000000000000000ull;
-        const uint32_t n = r - l;
-        const uint32_t nf = (n + 1u) >> 1, nb = n - nf;
-        // front chain state: A = [l, m), B = [m, r), windows a0..a3 / b0..b3
-        uint32_t ia = l, ib = m;
-        auto ldA = [&](uint32_t i) -> long long { return i < m ? (long long)src[i] : PINF; };
-        auto ldB = [&](uint32_t i) -> long long { return i < r ? (long long)src[i] : PINF; };
-        long long a0 = ldA(ia), a1 = ldA(ia + 1), a2 = ldA(ia + 2), a3 = ldA(ia + 3);
-        long long b0 = ldB(ib), b1 = ldB(ib + 1), b2 = ldB(ib + 2), b3 = ldB(ib + 3);
-        // back chain state: A' = A from the top, B' = B from the top
-        int32_t ja = (int32_t)m - 1, jb = (int32_t)r - 1;
-        auto ldA2 = [&](int32_t i) -> long long { return i >= (int32_t)l ? (long long)src[i] : NINF; };
-        auto ldB2 = [&](int32_t i) -> long long { return i >= (int32_t)m ? (long long)src[i] : NINF; };
-        long long c0 = ldA2(ja), c1 = ldA2(ja - 1), c2 = ldA2(ja - 2), c3 = ldA2(ja - 3);
-        long long e0 = ldB2(jb), e1 = ldB2(jb - 1), e2 = ldB2(jb - 2), e3 = ldB2(jb - 3);
-        uint32_t kf = l;
-        uint32_t kb = r - 1u;
-        for (uint32_t s = 0; s < nb; ++s) {
-            // front: take B only if strictly smaller (stable: left first on ties)
-            if (b0 < a0) {
-                dst[kf] = (int32_t)b0;
-                b0 = b1; b1 = b2; b2 = b3;
-                ++ib;
-                b3 = ldB(ib + 3);
-                if (((ib + 3) & 31u) == 0u && ib + 35 < r) asm volatile("prefetch.global.L1 [%0];" ::"l"(src + ib + 35));
-            } else {
-                dst[kf] = (int32_t)a0;
-                a0 = a1; a1 = a2; a2 = a3;
-                ++ia;
-                a3 = ldA(ia + 3);
-                if (((ia + 3) & 31u) == 0u && ia + 35 < m) asm volatile("prefetch.global.L1 [%0];" ::"l"(src + ia + 35));
-            }
-            ++kf;
-            // back: take A only if strictly larger (stable: right last on ties)
-            if (c0 > e0) {
-                dst[kb] = (int32_t)c0;
-                c0 = c1; c1 = c2; c2 = c3;
-                --ja;
-                c3 = ldA2(ja - 3);
-                if (((uint32_t)(ja - 3) & 31u) == 31u && ja - 35 >= (int32_t)l) asm volatile("prefetch.global.L1 [%0];" ::"l"(src + ja - 35));
-            } else {
-                dst[kb] = (int32_t)e0;
-                e0 = e1; e1 = e2; e2 = e3;
-                --jb;
-                e3 = ldB2(jb - 3);
-                if (((uint32_t)(jb - 3) & 31u) == 31u && jb - 35 >= (int32_t)m) asm volatile("prefetch.global.L1 [%0];" ::"l"(src + jb - 35));
-            }
-            --kb;
-        }
-        if (nf > nb) dst[kf] = (int32_t)(b0 < a0 ? b0 : a0);
+    __device__ __forceinline__ static void merge(const int32_t* src, int32_t* dst, uint32_t l, uint32_t m,
+                                                 uint32_t r) {
+        ms_merge(src, dst, l, m, r);
     }
 
     __device__ __forceinline__ static void exec(const Args& a, uint32_t fn, uint32_t state,

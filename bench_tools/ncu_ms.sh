@@ -2,5 +2,5 @@
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 timeout -s KILL 600 ncu --set full --import-source on --clock-control none -k regex:thread_sched -s 1 -c 1 \
-   -o gpurun_out/prof_ms --force-overwrite python bench_tools/profile_one.py ms 1048576 2 > gpurun_out/ncu_ms.log 2>&1
+   -o gpurun_out/prof_ms2 --force-overwrite python bench_tools/profile_one.py ms 1048576 2 > gpurun_out/ncu_ms.log 2>&1
 tail -3 gpurun_out/ncu_ms.log

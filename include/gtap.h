@@ -80,6 +80,8 @@ typedef struct {
     uint32_t max_roots;            /* forest capacity (roots per run); 0 = 65536 */
     uint64_t seed;                 /* victim-selection PRNG seed */
     uint64_t watchdog_ns;          /* 0 = off; else a run longer than this fails with GTAP_E_TIMEOUT */
+    uint32_t idle_backoff_ns;      /* cap of an idle worker's exponential nanosleep backoff; 0 = 8192 */
+    uint32_t reserved1;
 } gtap_config;
 
 typedef struct gtap_runtime gtap_runtime;

@@ -32,17 +32,22 @@ def _digest() -> str:
             if f.endswith((".cu", ".cuh", ".h")):
                 with open(os.path.join(d, f), "rb") as fh:
                     h.update(f.encode() + fh.read())
-    h.update(" ".join(ARCH + FLAGS).encode())
+    h.update(" ".join(ARCH + FLAGS).encode() + LIB.encode())
     return h.hexdigest()
 
 
-def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False, defines=(), out=None) -> str:
+    """Compile every .cu in SOURCES and link libgtap.so (out/defines: diagnostic variants only)."""
+    global LIB, BUILD
+    if defines or out:
+        LIB = out or LIB.replace(".so", "_" + "_".join(d.lower() for d in defines) + ".so")
+        BUILD = BUILD + "_" + "_".join(d.lower() for d in defines)
     os.makedirs(BUILD, exist_ok=True)
     stamp = os.path.join(BUILD, "stamp")
     dig = _digest()
     if not force and os.path.exists(LIB) and os.path.exists(stamp) and open(stamp).read() == dig:
         return LIB
-    extra = ["-Xptxas", "-v"] if ptxas_v else []
+    extra = (["-Xptxas", "-v"] if ptxas_v else []) + [f"-D{d}" for d in defines]
 
     def compile_one(src):
         obj = os.path.join(BUILD, src.replace(".cu", ".o"))
@@ -69,4 +74,5 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> 
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True, ptxas_v="-v" in sys.argv))
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    print(build(force="--force" in sys.argv, verbose=True, ptxas_v="-v" in sys.argv, defines=defs))

@@ -101,7 +101,7 @@ struct KParams {
     uint32_t steal_max;      // max tasks per steal
     uint32_t nroots;
     uint32_t max_child;      // GTAP_MAX_CHILD_TASKS (runtime check)
-    uint32_t pad;
+    uint32_t idle_backoff;   // max idle nanosleep (ns)
     unsigned long long seed;
     unsigned long long watchdog_ns;
     TaskRec* rec;            // W << logM records

@@ -71,6 +71,8 @@ gtap_status resolve(const gtap_config* in, gtap_config* c, int sm_count) {
     if (c->worker_kind == GTAP_WORKER_THREAD && c->steal_max > 32) return GTAP_E_INVAL;
     if (c->worker_kind == GTAP_WORKER_BLOCK && c->steal_max != 1) return GTAP_E_INVAL;
     if (c->max_roots == 0) c->max_roots = 65536;
+    if (c->idle_backoff_ns == 0) c->idle_backoff_ns = 8192;
+    if (c->idle_backoff_ns < 32 || c->idle_backoff_ns > 1000000) return GTAP_E_INVAL;
     const uint32_t wpb = (c->worker_kind == GTAP_WORKER_THREAD) ? c->block_size / 32 : 1;
     uint64_t W;
     if (c->grid_size) W = (uint64_t)c->grid_size * wpb;
@@ -288,6 +290,7 @@ gtap_status gtap_run(gtap_runtime* rt, void* stream) {
     p.max_child = rt->cfg.max_child_tasks ? rt->cfg.max_child_tasks : rt->table->max_children;
     p.seed = rt->cfg.seed;
     p.watchdog_ns = rt->cfg.watchdog_ns;
+    p.idle_backoff = rt->cfg.idle_backoff_ns;
     p.rec = reinterpret_cast<gtap::TaskRec*>(rt->ws + rt->L.rec);
     p.ring = reinterpret_cast<uint32_t*>(rt->ws + rt->L.ring);
     p.dq = reinterpret_cast<gtap::DequeMeta*>(rt->ws + rt->L.dq);

@@ -257,7 +257,8 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) block_sched_ker
                 id = __shfl_sync(0xffffffffu, got, 0);
                 if (id != kNone && lane == 0) ++L.st[ST_POPS];
                 // steal one from the fullest of 32 random victims
-                for (uint32_t round = 0; id == kNone && round < p.steal_rounds && p.W > 1; ++round) {
+                const uint32_t rounds = L.backoff >= 4096u ? 1u : p.steal_rounds;
+                for (uint32_t round = 0; id == kNone && round < rounds && p.W > 1; ++round) {
                     uint32_t v = xorshift32(L.rng) % (p.W - 1u);
                     v += (v >= w);
                     const unsigned long long sv = ld_relaxed(&p.dq[v].S);
@@ -310,7 +311,7 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) block_sched_ker
                 if (d && lane == 0) sm.exit_flag = 1;
                 if (!d) {
                     nanosleep(L.backoff);
-                    L.backoff = min(L.backoff * 2u, 2048u);
+                    L.backoff = min(L.backoff * 2u, p.idle_backoff);
                 }
             }
             if (lane == 0) sm.task_id = id;

@@ -57,6 +57,22 @@ struct TOut {
     __device__ __forceinline__ void bad_state() { action = kFinish; err = GTAP_E_BAD_STATE; }
 };
 
+constexpr uint32_t kHeavyBit = 0x80000000u;  // transient flag on runnable IDs (IDs < 2^31)
+
+// Placement hint (semantics-free, like EPAQ's queue choice P:990): a table may
+// mark tasks "heavy" (e.g. a mergesort subtree whose merges are large) so the
+// scheduler never keeps two of them in one warp.
+template <class T>
+__device__ __forceinline__ bool task_is_heavy(uint32_t fn, const uint32_t* d) {
+    if constexpr (T::kHasHeavy) return T::heavy(fn, d);
+    else return false;
+}
+template <class T>
+__device__ __forceinline__ bool parent_is_heavy(uint32_t child_fn, const uint32_t* child_d) {
+    if constexpr (T::kHasHeavy) return T::heavy_parent(child_fn, child_d);
+    else return false;
+}
+
 template <int MAXC>
 struct WarpSmem {
     uint32_t kept[32];          // keep-for-next-cycle set
@@ -65,6 +81,11 @@ struct WarpSmem {
     uint32_t cbuf[32 * MAXC];   // child IDs spawned this cycle, spawn order
     uint32_t pbuf[32];          // parents made runnable this cycle
 };
+
+template <class T>
+__host__ __device__ constexpr size_t block_extra_bytes() {
+    return (sizeof(typename T::BlockExtra) + 127) / 128 * 128;
+}
 
 template <class T>
 __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_kernel(KParams p, typename T::Args args) {
@@ -76,8 +97,12 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t wib = threadIdx.x >> 5;
     const uint32_t w = blockIdx.x * (blockDim.x >> 5) + wib;
+    // dynamic smem: [per-block table scratch (e.g. TMA merge slot)] [per-warp scheduler buffers]
+    typename T::BlockExtra* bx = reinterpret_cast<typename T::BlockExtra*>(smem_raw);
+    if (threadIdx.x == 0) T::block_init(bx);
+    __syncthreads();
     if (w >= p.W) return;  // whole warp
-    WarpSmem<MAXC>& sm = reinterpret_cast<WarpSmem<MAXC>*>(smem_raw)[wib];
+    WarpSmem<MAXC>& sm = reinterpret_cast<WarpSmem<MAXC>*>(smem_raw + block_extra_bytes<T>())[wib];
 
     const uint32_t M = 1u << p.logM, mmask = M - 1u;
     const uint32_t Q = p.qmask + 1u, qmask = p.qmask;
@@ -124,7 +149,7 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
     while (true) {
         // ================= (1) acquire =================
         uint32_t n = nkept;
-        uint32_t my = (lane < n) ? sm.kept[lane] : kNone;
+        uint32_t my = (lane < n) ? (sm.kept[lane] & ~kHeavyBit) : kNone;
         unsigned long long S_seen = 0;
         uint32_t done_seen = 0;
         if (lane == 0) {
@@ -152,7 +177,8 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
                     const uint32_t h = (uint32_t)s, sp = (uint32_t)(s >> 32);
                     const uint32_t avail = sp - h;
                     if (avail == 0u || avail > Q) break;
-                    const uint32_t c = min(32u, avail);
+                    // a small public part (top-of-tree / heavy tasks) is shared: take half (>= 1)
+                    const uint32_t c = avail <= 4u ? max(1u, avail >> 1) : min(32u, avail);
                     const unsigned long long nw = ((unsigned long long)(sp - c) << 32) | h;
                     const unsigned long long o = atom_cas_relaxed(&mydq->S, s, nw);
                     if (o == s) { got = c; s_new = sp - c; break; }
@@ -171,7 +197,9 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
         }
         // steal: probe 32 random victims in parallel, claim from the fullest
         if (n == 0 && p.W > 1) {
-            for (uint32_t round = 0; round < p.steal_rounds && n == 0; ++round) {
+            // a long-idle warp probes once per wake-up (keeps idle L2 traffic off busy workers)
+            const uint32_t rounds = backoff >= 4096u ? 1u : p.steal_rounds;
+            for (uint32_t round = 0; round < rounds && n == 0; ++round) {
                 uint32_t v = xorshift32(rng) % (p.W - 1u);
                 v += (v >= w);
                 const unsigned long long sv = ld_relaxed(&p.dq[v].S);
@@ -193,7 +221,8 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
                             const uint32_t h = (uint32_t)s, sp = (uint32_t)(s >> 32);
                             const uint32_t a = sp - h;
                             if (a == 0u || a > Q) break;
-                            const uint32_t c = min(p.steal_max, a);
+                            // claim up to steal_max; half of a small public part
+                            const uint32_t c = a <= 4u ? (a + 1u) >> 1 : min(p.steal_max, a);
                             const unsigned long long nw = ((unsigned long long)sp << 32) | (uint32_t)(h + c);
                             const unsigned long long o = atom_cas_acquire(&vdq->S, s, nw);
                             if (o == s) { got = c; h0 = h; break; }
@@ -230,7 +259,7 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
             if (d) break;
             if (p.watchdog_ns && lane == 0 && globaltimer() - t0 > p.watchdog_ns) raise_error(p.ctl, GTAP_E_TIMEOUT);
             nanosleep(backoff);
-            backoff = min(backoff * 2u, 2048u);
+            backoff = min(backoff * 2u, p.idle_backoff);
             continue;
         }
         backoff = 32;
@@ -240,15 +269,17 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
         Out o;
         o.init();
         uint32_t parent = kNone, aux = 0, ord = 0, myfn = 0;
+        uint32_t mydata[kDataWords] = {0, 0, 0, 0};
         if (my != kNone) {
             const uint4 h = ld_relaxed_v4(p.rec + my);
             const uint4 dv = ld_relaxed_v4(&p.rec[my].d[0]);
             const uint32_t d[kDataWords] = {dv.x, dv.y, dv.z, dv.w};
+            if (T::kHasHeavy) { mydata[0] = dv.x; mydata[1] = dv.y; mydata[2] = dv.z; mydata[3] = dv.w; }
             parent = h.z;
             aux = h.w;
             ord = meta_ord(h.x);
             myfn = meta_fn(h.x);
-            T::exec(args, meta_fn(h.x), meta_state(h.x), d, o);
+            T::exec(args, meta_fn(h.x), meta_state(h.x), d, o, bx);
             if (o.action == 0u) o.err = GTAP_E_BAD_STATE;
         }
         __syncwarp();
@@ -303,7 +334,7 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
                     TaskRec* cr = p.rec + cid;
                     st_v4(cr, make_uint4(make_meta(o.cfn[c], 0, c, 0), 0u, T::kTaskwait ? my : kNone, 0u));
                     st_v4(&cr->d[0], make_uint4(o.cd[c][0], o.cd[c][1], o.cd[c][2], o.cd[c][3]));
-                    sm.cbuf[g] = cid;
+                    sm.cbuf[g] = cid | (task_is_heavy<T>(o.cfn[c], o.cd[c]) ? kHeavyBit : 0u);
                 }
             }
         }
@@ -311,7 +342,7 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
         uint32_t resume_id = kNone;
         if (o.action == Out::kSuspend) {
             st_v2(p.rec + my, make_meta(myfn, o.next_state, ord, 0), nc);
-            if (nc == 0u) resume_id = my;  // empty join: runnable at once
+            if (nc == 0u) resume_id = my | (task_is_heavy<T>(myfn, mydata) ? kHeavyBit : 0u);  // empty join
         }
         // surplus freed records go back to their home worker's free ring
         if (F > T_total) {
@@ -340,7 +371,7 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
         if (fin && err == 0u) {
             if (parent != kNone) {
                 const int32_t old = atom_add_acq_rel(&p.rec[parent].pending, -1);
-                if (old == 1) resume_id = parent;
+                if (old == 1) resume_id = parent | (parent_is_heavy<T>(myfn, mydata) ? kHeavyBit : 0u);
             } else if (aux & kRootFlag) {
                 const uint32_t r = aux & ~kRootFlag;
                 p.root_results[r] = o.has_result ? (long long)o.result : 0ll;
@@ -368,32 +399,60 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
         if (resume_id != kNone) sm.pbuf[__popc(rball & lt)] = resume_id;
         __syncwarp();
         const uint32_t R = P + T_total;
-        const uint32_t keep = min(R, 32u);
-        uint32_t pushc = R - keep;
-        if (pushc) {
+        // keep <= 32 runnable tasks (resumed parents first, then children); tasks the table
+        // marks heavy are never kept: they are pushed and published so idle warps take them
+        uint32_t keep = 0, pushc = 0, heavy_pushed = 0;
+        for (uint32_t base = 0; base < R; base += 32) {
+            const uint32_t i = base + lane;
+            uint32_t id = kNone;
+            if (i < R) id = (i < P) ? sm.pbuf[i] : sm.cbuf[i - P];
+            const bool hv = (i < R) && (id & kHeavyBit);
+            const uint32_t light = __ballot_sync(0xffffffffu, i < R && !hv);
+            const uint32_t lrank = keep + __popc(light & lt);
+            const bool k = (i < R) && !hv && lrank < 32u;
+            const uint32_t kb = __ballot_sync(0xffffffffu, k);
+            const uint32_t pb = __ballot_sync(0xffffffffu, i < R && !k);
+            if (k) sm.kept[lrank] = id;
+            if (i < R && !k) {
+                const uint32_t slot = tail + pushc + __popc(pb & lt);
+                if (slot - sdone < Q) ring[slot & qmask] = id & ~kHeavyBit;
+            }
+            keep += __popc(kb);
+            pushc += __popc(pb);
+            heavy_pushed |= __ballot_sync(0xffffffffu, hv);
+        }
+        if (pushc && tail + pushc - sdone > Q) {
+            if (lane == 0) sdone = ld_relaxed(&mydq->steal_done);
+            sdone = __shfl_sync(0xffffffffu, sdone, 0);
             if (tail + pushc - sdone > Q) {
-                if (lane == 0) sdone = ld_relaxed(&mydq->steal_done);
-                sdone = __shfl_sync(0xffffffffu, sdone, 0);
-                if (tail + pushc - sdone > Q) {
-                    if (lane == 0) raise_error(p.ctl, GTAP_E_QUEUE_OVERFLOW);
-                    break;
-                }
+                if (lane == 0) raise_error(p.ctl, GTAP_E_QUEUE_OVERFLOW);
+                break;
+            }
+            // capacity was only stale: write the entries skipped above
+            for (uint32_t base = 0, kk = 0, pc = 0; base < R; base += 32) {
+                const uint32_t i = base + lane;
+                uint32_t id = kNone;
+                if (i < R) id = (i < P) ? sm.pbuf[i] : sm.cbuf[i - P];
+                const bool hv = (i < R) && (id & kHeavyBit);
+                const uint32_t light = __ballot_sync(0xffffffffu, i < R && !hv);
+                const bool k = (i < R) && !hv && (kk + __popc(light & lt)) < 32u;
+                const uint32_t pb = __ballot_sync(0xffffffffu, i < R && !k);
+                if (i < R && !k) ring[(tail + pc + __popc(pb & lt)) & qmask] = id & ~kHeavyBit;
+                kk += __popc(__ballot_sync(0xffffffffu, k));
+                pc += __popc(pb);
             }
         }
-        for (uint32_t i = lane; i < R; i += 32) {
-            const uint32_t id = (i < P) ? sm.pbuf[i] : sm.cbuf[i - P];
-            if (i < keep) sm.kept[i] = id;
-            else ring[(tail + (i - keep)) & qmask] = id;
-        }
+        __syncwarp();
         tail += pushc;
         nkept = keep;
         if (lane == 0) st_push += pushc;
-        // publish the oldest half of the private part when thieves drained the public part
+        // publish the oldest half of the private part when thieves drained the public part,
+        // or everything at once when heavy tasks were just pushed
         if (lane == 0) {
             const uint32_t h = (uint32_t)S_seen;
             const uint32_t priv = tail - split;
-            if (h == split && priv >= 2u) {
-                const uint32_t k = priv >> 1;
+            if ((heavy_pushed && priv) || (h == split && priv >= 2u)) {
+                const uint32_t k = heavy_pushed ? priv : (priv >> 1);
                 split += k;
                 red_add_release(&mydq->S, (unsigned long long)k << 32);
             }

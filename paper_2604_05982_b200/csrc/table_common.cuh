@@ -27,7 +27,7 @@ namespace gtap {
 
 template <class T>
 inline size_t thread_smem(uint32_t block) {
-    return (size_t)(block / 32) * sizeof(WarpSmem<T::kMaxChildren>);
+    return block_extra_bytes<T>() + (size_t)(block / 32) * sizeof(WarpSmem<T::kMaxChildren>);
 }
 
 template <class T>
@@ -36,6 +36,10 @@ cudaError_t launch_thread(const gtap_task_table* t, const KParams& p, uint32_t g
     typename T::Args a;
     std::memcpy(&a, t->args, sizeof(a));
     const size_t smem = thread_smem<T>(block);
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(thread_sched_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
     thread_sched_kernel<T><<<grid, block, smem, s>>>(p, a);
     return cudaGetLastError();
 }
@@ -43,6 +47,10 @@ cudaError_t launch_thread(const gtap_task_table* t, const KParams& p, uint32_t g
 template <class T>
 cudaError_t occupancy_thread(const gtap_task_table*, uint32_t block, int* bps, size_t* smem) {
     *smem = thread_smem<T>(block);
+    if (*smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(thread_sched_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem);
+        if (e != cudaSuccess) return e;
+    }
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, thread_sched_kernel<T>, (int)block, *smem);
 }
 

@@ -15,13 +15,19 @@ struct FibTable {
     static constexpr uint32_t kKind = GTAP_WORKER_THREAD;
     static constexpr int kMaxChildren = 2;
     static constexpr bool kTaskwait = true;
+    static constexpr bool kHasHeavy = false;
     static constexpr uint32_t kNumFn = 1;
     static constexpr int kMaxThreads = 256, kMinBlocks = 4;  // __launch_bounds__
     struct Args {
         uint32_t unused;
     };
+    struct BlockExtra {
+        uint32_t unused;
+    };
+    __device__ __forceinline__ static void block_init(BlockExtra*) {}
     __device__ __forceinline__ static void exec(const Args&, uint32_t fn, uint32_t state,
-                                                const uint32_t (&d)[kDataWords], TOut<kMaxChildren>& o) {
+                                                const uint32_t (&d)[kDataWords], TOut<kMaxChildren>& o,
+                                                BlockExtra*) {
         if (fn != 0u) { o.bad_state(); return; }
         switch (state) {
             case 0: {

@@ -15,6 +15,8 @@
 // written exactly once per tree level (8 B/key/level, no copy-back), and the
 // root (depth 0) ends in `keys`. The output is the unique sorted permutation
 // either way. Payload: d[0] = l, d[1] = r, d[2] = depth.
+#include <climits>
+
 #include "table_common.cuh"
 
 namespace gtap {
@@ -85,18 +87,482 @@ __device__ __noinline__ void ms_merge(const int32_t* __restrict__ src, int32_t* 
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// TMA-staged single-thread merge (B200 path for large merges).
+//
+// Calibration on B200 (profiles/r01_calib_single_thread.txt): one thread
+// streaming 4-byte global loads sustains only ~13.5 ns per load even when the
+// loads are independent and L2-resident, while shared-memory loads cost ~15 ns
+// dependent and far less pipelined. So the thread that runs a large merge
+// streams its two runs (from both ends) through shared memory with 1-D bulk
+// TMA copies (cp.async.bulk, mbarrier completion), and streams its two output
+// halves back with bulk stores: the thread then only issues one bulk copy per
+// 512 keys per stream and merges out of shared memory. One 24 KB merge slot
+// per block; a lane claims it with a shared-memory CAS, other lanes use
+// ms_merge. Partial chunks at the ends of the output range are written with
+// plain stores (a bulk store must not touch a neighbouring task's keys).
+namespace tma {
+__device__ __forceinline__ uint32_t sa(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* mb, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sa(mb)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* mb, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(mb)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* mb, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred P;\n"
+        "GTAP_WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+        " @!P bra GTAP_WAIT_%=;\n}" ::"r"(sa(mb)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* mb) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(sa(dst)),
+                 "l"(src), "r"(bytes), "r"(sa(mb)) : "memory");
+}
+__device__ __forceinline__ void s2g(void* dst, const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(sa(src)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void wait_read(uint32_t n) {  // <= n most recent bulk groups may still read smem
+    if (n == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    else if (n == 1) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+    else if (n == 2) asm volatile("cp.async.bulk.wait_group.read 2;" ::: "memory");
+    else asm volatile("cp.async.bulk.wait_group.read 3;" ::: "memory");
+}
+__device__ __forceinline__ void wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void fence_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+}  // namespace tma
+
+__device__ __forceinline__ int32_t lds(uint32_t a) {
+    int32_t v;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts(uint32_t a, int32_t v) {
+    asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
+#ifdef GTAP_MS_PROBE_STATS
+__device__ long long gtap_ms_probe[8];
+extern "C" int gtap_ms_probe_read(long long* h) {
+    cudaMemcpyFromSymbol(h, gtap_ms_probe, sizeof(long long) * 8);
+    long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(gtap_ms_probe, z, sizeof(z));
+    return 0;
+}
+#endif
+
+#ifndef GTAP_MS_CHAINS
+#define GTAP_MS_CHAINS 4
+#endif
+constexpr int kChains = GTAP_MS_CHAINS;      // independent merge chains interleaved in one thread
+constexpr int kIn = 256;                     // keys per input chunk (1 KB bulk load)
+constexpr int kOut = 128;                    // keys per output chunk (512 B bulk store)
+constexpr int kRing = 512;                   // keys per ring (2 input chunks / 4 output chunks), 2 KB
+constexpr uint32_t kRingMaskB = kRing * 4u - 1u;
+constexpr uint32_t kTmaMin = 8192;           // merges at least this long take the TMA path
+constexpr uint32_t kNoChunk = 0x80000000u;
+#ifdef GTAP_MS_TRACE
+__device__ ulonglong4 gtap_ms_trace[65536];
+__device__ uint32_t gtap_ms_trace_n;
+extern "C" int gtap_ms_trace_read(void* host, uint32_t* n) {
+    cudaMemcpyFromSymbol(n, gtap_ms_trace_n, 4);
+    cudaMemcpyFromSymbol(host, gtap_ms_trace, sizeof(ulonglong4) * (*n < 65536u ? *n : 65536u));
+    const uint32_t z = 0;
+    cudaMemcpyToSymbol(gtap_ms_trace_n, &z, 4);
+    return 0;
+}
+#endif
+
+struct MergeSlot {                           // placed 2 KB-aligned inside the block's dynamic smem
+    int32_t in[2 * kChains][kRing];          // per chain: A ring, B ring
+    int32_t out[kChains][kRing];             // per chain: output ring
+    unsigned long long mbar[2 * kChains][2];
+    uint32_t par[2 * kChains];               // mbarrier parity bits per input ring
+};
+struct MergeSlotHolder {                     // BlockExtra: 2 KB of slack to align the slot
+    unsigned char raw[sizeof(MergeSlot) + 2048];
+    uint32_t busy;
+    __device__ __forceinline__ MergeSlot* slot() {
+        const uint32_t a = tma::sa(raw);
+        return reinterpret_cast<MergeSlot*>(raw + ((2048u - (a & 2047u)) & 2047u));
+    }
+};
+
+__device__ __forceinline__ bool mbar_try(uint32_t mb, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred P;\n mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n selp.u32 %0, 1, 0, P;\n}"
+        : "=r"(ok) : "r"(mb), "r"(parity) : "memory");
+    return ok != 0;
+}
+
+// Input run streamed through a 2-chunk ring. Up streams hold the resident window
+// [chunk(pos)*kIn, rhi); down streams (rlo, ...] mirrored with rhi = lowest resident key.
+struct InS {
+    const int32_t* g;
+    uint32_t ring;        // smem byte address (2 KB aligned)
+    uint32_t mb;          // smem byte address of 2 mbarriers
+    int32_t pos, lo, hi;  // head, run [lo, hi)
+    int32_t edge;         // up: resident end (exclusive); down: lowest resident key
+    uint32_t pend;        // chunk in flight or kNoChunk
+    uint32_t par;
+    int32_t nt;
+};
+__device__ __forceinline__ void in_issue(InS& s, int32_t c) {
+    const int32_t b0 = c * kIn;
+    const uint32_t bytes = (uint32_t)min(kIn, s.nt - b0) * 4u;
+    const uint32_t sl = (uint32_t)c & 1u;
+    tma::fence_smem();
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s.mb + 8u * sl), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(s.ring + sl * (kIn * 4u)), "l"(s.g + b0), "r"(bytes), "r"(s.mb + 8u * sl) : "memory");
+    s.pend = (uint32_t)c;
+}
+__device__ __forceinline__ bool in_poll(InS& s, bool block) {  // true if the pending chunk landed
+    const uint32_t sl = s.pend & 1u;
+    const uint32_t ph = (s.par >> sl) & 1u;
+    if (block) {
+        while (!mbar_try(s.mb + 8u * sl, ph)) {}
+    } else if (!mbar_try(s.mb + 8u * sl, ph)) {
+        return false;
+    }
+    s.par ^= 1u << sl;
+    s.pend = kNoChunk;
+    return true;
+}
+__device__ __forceinline__ void in_start(InS& s, bool up) {
+    s.pend = kNoChunk;
+    if (s.lo >= s.hi) { s.edge = up ? s.hi : s.lo; return; }
+    const int32_t c = s.pos / kIn;
+    in_issue(s, c);
+    in_poll(s, true);
+    s.edge = up ? (c + 1) * kIn : c * kIn;
+}
+// keep the window full: land a pending chunk, issue the next one into the free slot
+// (issue first: a head that left the window gets its chunk requested and waited here)
+__device__ __forceinline__ void in_maint(InS& s, bool up) {
+    if (up) {
+        if (s.pend == kNoChunk && s.edge < s.hi && s.edge - s.pos <= kIn) in_issue(s, s.edge / kIn);
+        if (s.pend != kNoChunk && in_poll(s, s.pos + 1 >= s.edge)) s.edge += kIn;
+    } else {
+        if (s.pend == kNoChunk && s.edge > s.lo && s.pos - s.edge < kIn) in_issue(s, s.edge / kIn - 1);
+        if (s.pend != kNoChunk && in_poll(s, s.pos - 1 < s.edge)) s.edge -= kIn;
+    }
+}
+__device__ __forceinline__ int32_t in_safe(const InS& s, bool up) {
+    return up ? min(s.edge, s.hi) - 1 - s.pos : s.pos - max(s.edge, s.lo);
+}
+__device__ __forceinline__ uint32_t in_addr(const InS& s, int32_t p) {
+    return s.ring + (((uint32_t)p * 4u) & kRingMaskB);
+}
+
+// Output range streamed through a 4-chunk ring; completed chunks leave by bulk store
+// (or plain stores for a chunk that is only partly inside [lo, hi)).
+struct OutS {
+    int32_t* g;
+    uint32_t ring;
+    int32_t pos, lo, hi;  // next position, range
+    int32_t fl;           // next chunk to flush
+    int32_t wend;         // up: writable end (exclusive); down: lowest writable key
+    uint32_t gid[4];
+};
+__device__ __forceinline__ void out_flush(OutS& o, int32_t c, uint32_t& gc) {
+    const int32_t b0 = c * kOut;
+    const int32_t cs = max(b0, o.lo), ce = min(b0 + kOut, o.hi);
+    const uint32_t sb = o.ring + ((uint32_t)(c & 3)) * (kOut * 4u);
+    if (cs == b0 && ce == b0 + kOut) {
+        tma::fence_smem();
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(o.g + b0), "r"(sb),
+                     "r"(kOut * 4u) : "memory");
+        tma::commit();
+        o.gid[c & 3] = ++gc;
+    } else {
+        for (int32_t i = cs; i < ce; ++i) o.g[i] = lds(sb + 4u * (uint32_t)(i - b0));
+    }
+}
+__device__ __forceinline__ void out_claim(OutS& o, int32_t c, uint32_t gc) {  // slot of chunk c free to write
+    const uint32_t gid = o.gid[c & 3];
+    if (gid) { tma::wait_read(min(gc - gid, 3u)); o.gid[c & 3] = 0; }
+}
+__device__ __forceinline__ void out_start(OutS& o, bool up, uint32_t gc) {
+    o.gid[0] = o.gid[1] = o.gid[2] = o.gid[3] = 0;
+    if (up) { o.pos = o.lo; o.fl = o.lo / kOut; o.wend = (o.fl + 1) * kOut; }
+    else    { o.pos = o.hi - 1; o.fl = o.hi > 0 ? (o.hi - 1) / kOut : 0; o.wend = o.fl * kOut; }
+    (void)gc;
+}
+__device__ __forceinline__ void out_maint(OutS& o, bool up, uint32_t& gc) {
+    if (up) {
+        while (o.fl * kOut < o.hi && ((o.fl + 1) * kOut <= o.pos || o.pos == o.hi)) { out_flush(o, o.fl, gc); ++o.fl; }
+        while (o.wend < o.hi && o.wend / kOut < o.fl + 3) { out_claim(o, o.wend / kOut, gc); o.wend += kOut; }
+    } else {
+        while (o.fl >= 0 && (o.fl + 1) * kOut > o.lo && (o.fl * kOut > o.pos || o.pos < o.lo)) {
+            out_flush(o, o.fl, gc);
+            --o.fl;
+        }
+        while (o.wend > o.lo && o.wend / kOut - 1 > o.fl - 3) { out_claim(o, o.wend / kOut - 1, gc); o.wend -= kOut; }
+    }
+}
+__device__ __forceinline__ int32_t out_safe(const OutS& o, bool up) {
+    return up ? min(o.wend, o.hi) - o.pos : o.pos - max(o.wend, o.lo) + 1;
+}
+
+struct Chain {
+    InS A, B;
+    OutS O;
+    int32_t left;
+};
+
+// one checked step (exhausted runs read as 64-bit sentinels), used when a run is at its last key
+__device__ __forceinline__ void chain_step_checked(Chain& ch, bool up) {
+    InS& A = ch.A;
+    InS& B = ch.B;
+    if (up) {
+        const long long a = A.pos < A.hi ? (long long)lds(in_addr(A, A.pos)) : 0x7fffffffffffffffll;
+        const long long b = B.pos < B.hi ? (long long)lds(in_addr(B, B.pos)) : 0x7fffffffffffffffll;
+        const bool tb = b < a;
+        sts(ch.O.ring + (((uint32_t)ch.O.pos * 4u) & kRingMaskB), (int32_t)(tb ? b : a));
+        ++ch.O.pos;
+        if (tb) ++B.pos; else ++A.pos;
+    } else {
+        const long long a = A.pos >= A.lo ? (long long)lds(in_addr(A, A.pos)) : (long long)0x8000000000000000ull;
+        const long long b = B.pos >= B.lo ? (long long)lds(in_addr(B, B.pos)) : (long long)0x8000000000000000ull;
+        const bool ta = a > b;  // stable: left run only if strictly larger
+        sts(ch.O.ring + (((uint32_t)ch.O.pos * 4u) & kRingMaskB), (int32_t)(ta ? a : b));
+        --ch.O.pos;
+        if (ta) --A.pos; else --B.pos;
+    }
+    --ch.left;
+}
+
+// stable merge-path split: number of A keys among the first t outputs of merge(A, B)
+__device__ __forceinline__ uint32_t merge_path(const int32_t* src, uint32_t l, uint32_t m, uint32_t r, uint32_t t) {
+    uint32_t lo = t > (r - m) ? t - (r - m) : 0u, hi = min(t, m - l);
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (src[l + mid] <= src[m + (t - mid - 1)]) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+// Stable merge of src[l, m) and src[m, r) into dst[l, r) by ONE thread through
+// the block's merge slot (nt = array length, a multiple of 4; 16-B aligned).
+// The output is cut by merge-path searches into kChains/2 independent
+// sub-merges, each produced from both ends (an ascending and a descending
+// chain), so kChains dependency chains interleave in the hot loop. Between
+// stretches every stream is maintained (bulk loads landed/issued, output
+// chunks flushed by bulk store, output slots reclaimed); a stretch is as long
+// as every chain can go without reaching a window edge or a run end.
+// Returns false if the merge stopped making progress (a bug surfaced as GTAP_E_BAD_STATE).
+__device__ __noinline__ bool ms_merge_tma(const int32_t* src, int32_t* dst, uint32_t l, uint32_t m, uint32_t r,
+                                          uint32_t nt, MergeSlotHolder* H) {
+    bool ok = true;
+    MergeSlot* S = H->slot();
+    tma::fence_global();  // children's generic-proxy writes (acquired at the join) -> async-proxy reads
+    constexpr int kSub = kChains / 2;
+    const uint32_t n = r - l;
+    uint32_t cut_a[kSub + 1], cut_t[kSub + 1];
+#pragma unroll
+    for (int q = 0; q <= kSub; ++q) {
+        const uint32_t t = (uint32_t)(((unsigned long long)n * q) / kSub);
+        cut_t[q] = t;
+        cut_a[q] = (q == 0) ? 0u : (q == kSub ? m - l : merge_path(src, l, m, r, t));
+    }
+    Chain ch[kChains];
+    uint32_t gc = 0;
+#pragma unroll
+    for (int k = 0; k < kChains; ++k) {
+        const int q = k >> 1;
+        const bool up = (k & 1) == 0;
+        Chain& c = ch[k];
+        const int32_t alo = (int32_t)(l + cut_a[q]), ahi = (int32_t)(l + cut_a[q + 1]);
+        const int32_t blo = (int32_t)(m + cut_t[q] - cut_a[q]), bhi = (int32_t)(m + cut_t[q + 1] - cut_a[q + 1]);
+        const int32_t olo = (int32_t)(l + cut_t[q]), ohi = (int32_t)(l + cut_t[q + 1]);
+        const int32_t nq = ohi - olo, nf = (nq + 1) >> 1;
+        c.A.g = c.B.g = src;
+        c.A.nt = c.B.nt = (int32_t)nt;
+        c.A.ring = tma::sa(&S->in[2 * k][0]);
+        c.B.ring = tma::sa(&S->in[2 * k + 1][0]);
+        c.A.mb = tma::sa(&S->mbar[2 * k][0]);
+        c.B.mb = tma::sa(&S->mbar[2 * k + 1][0]);
+        c.A.par = S->par[2 * k];
+        c.B.par = S->par[2 * k + 1];
+        c.A.lo = alo; c.A.hi = ahi; c.B.lo = blo; c.B.hi = bhi;
+        c.A.pos = up ? alo : ahi - 1;
+        c.B.pos = up ? blo : bhi - 1;
+        c.O.g = dst;
+        c.O.ring = tma::sa(&S->out[k][0]);
+        c.O.lo = up ? olo : olo + nf;
+        c.O.hi = up ? olo + nf : ohi;
+        c.left = c.O.hi - c.O.lo;
+        in_start(c.A, up);
+        in_start(c.B, up);
+        out_start(c.O, up, gc);
+    }
+#ifdef GTAP_MS_PROBE_STATS
+    long long t_hot = 0, t_all0 = clock64(), n_str = 0, n_fast = 0, n_chk = 0;
+#endif
+    uint32_t stall = 0;
+    while (true) {
+        int32_t steps = 0x7fffffff;
+        int32_t work = 0, done_any = 0;
+#pragma unroll
+        for (int k = 0; k < kChains; ++k) {
+            work |= ch[k].left;
+            done_any |= (ch[k].left == 0);
+        }
+        if (work == 0) break;
+#pragma unroll
+        for (int k = 0; k < kChains; ++k) {
+            const bool up = (k & 1) == 0;
+            Chain& c = ch[k];
+            in_maint(c.A, up);
+            in_maint(c.B, up);
+            out_maint(c.O, up, gc);
+            steps = min(steps, min(min(in_safe(c.A, up), in_safe(c.B, up)), min(out_safe(c.O, up), c.left)));
+        }
+        if (steps <= 0 || done_any) {
+            // an edge (run end, ring wrap, window edge) or the last keys: one checked step on
+            // every chain that can write (heads are resident after in_maint)
+            bool moved = false;
+#pragma unroll
+            for (int k = 0; k < kChains; ++k) {
+                const bool up = (k & 1) == 0;
+                if (ch[k].left > 0 && out_safe(ch[k].O, up) > 0) {
+                    chain_step_checked(ch[k], up);
+                    moved = true;
+#ifdef GTAP_MS_PROBE_STATS
+                    ++n_chk;
+#endif
+                }
+            }
+            if (!moved && ++stall > (1u << 24)) {  // no chain could move for a long time: a bug, not a hang
+                ok = false;
+                break;
+            }
+            continue;
+        }
+        stall = 0;
+        // hot loop: `steps` unchecked steps on every chain; heads and outputs move through ring byte
+        // addresses (IADD + LOP3 each): per key 1 compare, 1 min/max, 1 st.shared, 2 ld.shared
+#ifdef GTAP_MS_PROBE_STATS
+        const long long th0 = clock64();
+        ++n_str; n_fast += steps;
+#endif
+        // tagged smem byte addresses: every ring is 2 KB and 2 KB-aligned, so a head moves by
+        // addr = ring | ((addr + 4) & mask): one IADD + one LOP3, and ld/st.shared use it directly
+        uint32_t ao[kChains], bo[kChains], oo[kChains];
+        int32_t av[kChains], bv[kChains];
+        int32_t da[kChains], db[kChains];
+#pragma unroll
+        for (int k = 0; k < kChains; ++k) {
+            ao[k] = ch[k].A.ring | (((uint32_t)ch[k].A.pos * 4u) & kRingMaskB);
+            bo[k] = ch[k].B.ring | (((uint32_t)ch[k].B.pos * 4u) & kRingMaskB);
+            oo[k] = ch[k].O.ring | (((uint32_t)ch[k].O.pos * 4u) & kRingMaskB);
+            av[k] = lds(ao[k]);
+            bv[k] = lds(bo[k]);
+            da[k] = db[k] = 0;
+            ch[k].left -= steps;
+        }
+#pragma unroll 4
+        for (int32_t st = 0; st < steps; ++st) {
+#pragma unroll
+            for (int k = 0; k < kChains; ++k) {
+                const uint32_t ra = ch[k].A.ring, rb = ch[k].B.ring, ro = ch[k].O.ring;
+                if ((k & 1) == 0) {  // ascending chain: right run only if strictly smaller
+                    const uint32_t d = bv[k] < av[k] ? 4u : 0u;
+#ifndef GTAP_MS_PROBE_NOSTORE
+                    sts(oo[k], min(av[k], bv[k]));
+#endif
+                    oo[k] = ro | ((oo[k] + 4u) & kRingMaskB);
+                    ao[k] = ra | ((ao[k] + 4u - d) & kRingMaskB);
+                    bo[k] = rb | ((bo[k] + d) & kRingMaskB);
+                    db[k] += (int32_t)d;
+                } else {             // descending chain: left run only if strictly larger
+                    const uint32_t d = av[k] > bv[k] ? 4u : 0u;
+#ifndef GTAP_MS_PROBE_NOSTORE
+                    sts(oo[k], max(av[k], bv[k]));
+#endif
+                    oo[k] = ro | ((oo[k] - 4u) & kRingMaskB);
+                    ao[k] = ra | ((ao[k] - d) & kRingMaskB);
+                    bo[k] = rb | ((bo[k] - 4u + d) & kRingMaskB);
+                    da[k] += (int32_t)d;
+                }
+                av[k] = lds(ao[k]);
+                bv[k] = lds(bo[k]);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < kChains; ++k) {
+            // up: B moved db/4 keys, A the rest; down: A moved da/4 keys, B the rest
+            if ((k & 1) == 0) {
+                ch[k].B.pos += db[k] / 4;
+                ch[k].A.pos += steps - db[k] / 4;
+                ch[k].O.pos += steps;
+            } else {
+                ch[k].A.pos -= da[k] / 4;
+                ch[k].B.pos -= steps - da[k] / 4;
+                ch[k].O.pos -= steps;
+            }
+        }
+#ifdef GTAP_MS_PROBE_STATS
+        t_hot += clock64() - th0 + (long long)(av[0] & 0);
+#endif
+    }
+#ifdef GTAP_MS_PROBE_STATS
+    if (n >= gtap_ms_probe[7]) {  // keep the stats of the largest merge
+        gtap_ms_probe[7] = n;
+        gtap_ms_probe[0] = clock64() - t_all0; gtap_ms_probe[1] = t_hot; gtap_ms_probe[2] = n_str;
+        gtap_ms_probe[3] = n_fast; gtap_ms_probe[4] = n_chk;
+    }
+#endif
+#pragma unroll
+    for (int k = 0; k < kChains; ++k) {
+        const bool up = (k & 1) == 0;
+        out_maint(ch[k].O, up, gc);  // flush the final (partial) chunks
+        if (ch[k].A.pend != kNoChunk) in_poll(ch[k].A, true);
+        if (ch[k].B.pend != kNoChunk) in_poll(ch[k].B, true);
+        S->par[2 * k] = ch[k].A.par;
+        S->par[2 * k + 1] = ch[k].B.par;
+    }
+    tma::wait_all();
+    tma::fence_global();  // async-proxy writes complete before the join's release
+    return ok;
+}
+
 struct MergesortTable {
     static constexpr uint32_t kKind = GTAP_WORKER_THREAD;
     static constexpr int kMaxChildren = 2;
     static constexpr bool kTaskwait = true;
     static constexpr uint32_t kNumFn = 1;
+    // placement hint: subtrees whose merges take the TMA path are spread over warps (never two
+    // in one warp's kept set, where they would share issue slots and the block's merge slot)
+    static constexpr bool kHasHeavy = true;
+    __device__ __forceinline__ static bool heavy(uint32_t, const uint32_t* d) { return d[1] - d[0] >= kTmaMin; }
+    __device__ __forceinline__ static bool heavy_parent(uint32_t, const uint32_t* d) {
+        return 2u * (d[1] - d[0]) >= kTmaMin;
+    }
     static constexpr int kMaxThreads = 128, kMinBlocks = 4;  // __launch_bounds__: 128 regs, no spills
     struct Args {
         int32_t* keys;
         int32_t* scratch;
         uint32_t cutoff;
-        uint32_t pad;
+        uint32_t n;         // array length (TMA path needs n % 4 == 0 and 16-B aligned buffers)
     };
+    using BlockExtra = MergeSlotHolder;
+    __device__ __forceinline__ static void block_init(BlockExtra* H) {
+        MergeSlot* S = H->slot();
+        for (int k = 0; k < 2 * kChains; ++k) {
+            for (int j = 0; j < 2; ++j) tma::mbar_init(&S->mbar[k][j], 1);
+            S->par[k] = 0;
+        }
+        H->busy = 0;
+        tma::fence_smem();
+    }
 
     __device__ __forceinline__ static int32_t* buf(const Args& a, uint32_t depth) {
         return (depth & 1u) ? a.scratch : a.keys;
@@ -120,13 +586,41 @@ struct MergesortTable {
     }
 
     // merge: stable merge of src[l, m) and src[m, r) into dst[l, r).
-    __device__ __forceinline__ static void merge(const int32_t* src, int32_t* dst, uint32_t l, uint32_t m,
-                                                 uint32_t r) {
-        ms_merge(src, dst, l, m, r);
+    __device__ __forceinline__ static bool merge(const Args& a, const int32_t* src, int32_t* dst, uint32_t l,
+                                                 uint32_t m, uint32_t r, MergeSlotHolder* S) {
+        const bool tma_ok = (r - l) >= kTmaMin && (a.n & 3u) == 0u &&
+                            ((reinterpret_cast<uintptr_t>(a.keys) | reinterpret_cast<uintptr_t>(a.scratch)) & 15u) == 0u;
+#ifdef GTAP_MS_TRACE
+        const unsigned long long t0 = dev::globaltimer();
+        uint32_t used = 0;
+#endif
+        bool ok = true;
+        if (tma_ok && atomicCAS(&S->busy, 0u, 1u) == 0u) {
+            ok = ms_merge_tma(src, dst, l, m, r, a.n, S);
+            atomicExch(&S->busy, 0u);
+#ifdef GTAP_MS_TRACE
+            used = 1;
+#endif
+        } else {
+            ms_merge(src, dst, l, m, r);
+        }
+#ifdef GTAP_MS_TRACE
+        if (r - l >= 4096u) {
+            const uint32_t i = atomicAdd(&gtap_ms_trace_n, 1u);
+            if (i < 65536u) {
+                unsigned smid;
+                asm("mov.u32 %0, %%smid;" : "=r"(smid));
+                gtap_ms_trace[i] = make_ulonglong4(t0, dev::globaltimer(), ((unsigned long long)(r - l) << 32) | l,
+                                                   ((unsigned long long)smid << 8) | used);
+            }
+        }
+#endif
+        return ok;
     }
 
     __device__ __forceinline__ static void exec(const Args& a, uint32_t fn, uint32_t state,
-                                                const uint32_t (&d)[kDataWords], TOut<kMaxChildren>& o) {
+                                                const uint32_t (&d)[kDataWords], TOut<kMaxChildren>& o,
+                                                BlockExtra* S) {
         if (fn != 0u) { o.bad_state(); return; }
         const uint32_t l = d[0], r = d[1], depth = d[2];
         switch (state) {
@@ -144,7 +638,7 @@ struct MergesortTable {
                 }
             case 1: {
                 const uint32_t m = l + (r - l) / 2u;
-                merge(buf(a, depth + 1u), buf(a, depth), l, m, r);
+                if (!merge(a, buf(a, depth + 1u), buf(a, depth), l, m, r, S)) { o.bad_state(); return; }
                 o.finish_void();
                 return;
             }
@@ -163,6 +657,6 @@ static int validate_ms(const gtap_task_table* t, uint32_t fn, const uint32_t* d)
 
 extern "C" const gtap_task_table* gtap_table_mergesort(int32_t* keys, int32_t* scratch, uint64_t n, int32_t cutoff) {
     if (((!keys || !scratch) && n > 0) || cutoff < 1 || cutoff > gtap::kMsMaxCutoff || n >= (1ull << 31)) return nullptr;
-    gtap::MergesortTable::Args a{keys, scratch, (uint32_t)cutoff, 0u};
+    gtap::MergesortTable::Args a{keys, scratch, (uint32_t)cutoff, (uint32_t)n};
     return gtap::make_table<gtap::MergesortTable>("mergesort", a, &gtap::validate_ms);
 }

@@ -13,7 +13,7 @@ import os
 from dataclasses import dataclass
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libgtap.so")
+LIB_PATH = os.environ.get("GTAP_LIB") or os.path.join(_PKG, "libgtap.so")  # GTAP_LIB: diagnostic builds
 
 GTAP_WORKER_THREAD = 0
 GTAP_WORKER_BLOCK = 1
@@ -40,6 +40,7 @@ class Config(ctypes.Structure):
         ("max_task_data_size", ctypes.c_uint32), ("assume_no_taskwait", ctypes.c_uint32),
         ("steal_attempts", ctypes.c_uint32), ("steal_max", ctypes.c_uint32), ("max_roots", ctypes.c_uint32),
         ("seed", ctypes.c_uint64), ("watchdog_ns", ctypes.c_uint64),
+        ("idle_backoff_ns", ctypes.c_uint32), ("reserved1", ctypes.c_uint32),
     ]
 
 
@@ -210,6 +211,7 @@ class Runtime:
     def __init__(self, kind: int, device: int = 0, *, grid_size: int = 0, block_size: int = 0,
                  max_tasks_per_worker: int = 0, queue_capacity: int = 0, steal_attempts: int = 0,
                  steal_max: int = 0, seed: int = 0x5EED, watchdog_ns: int = 0, max_roots: int = 0,
+                 idle_backoff_ns: int = 0,
                  torch_workspace: bool = True):
         import torch
         L = lib()
@@ -217,7 +219,7 @@ class Runtime:
         _check(L.gtap_config_default(ctypes.byref(cfg), device, kind), "gtap_config_default")
         for k, v in dict(grid_size=grid_size, block_size=block_size, max_tasks_per_worker=max_tasks_per_worker,
                          queue_capacity=queue_capacity, steal_attempts=steal_attempts, steal_max=steal_max,
-                         watchdog_ns=watchdog_ns, max_roots=max_roots).items():
+                         watchdog_ns=watchdog_ns, max_roots=max_roots, idle_backoff_ns=idle_backoff_ns).items():
             if v:
                 setattr(cfg, k, v)
         cfg.seed = seed

@@ -36,7 +36,10 @@ def run_sort(g, rt, keys_np, cutoff=128):
     return d.cpu().numpy(), st
 
 
-@pytest.mark.parametrize("n", [0, 1, 2, 31, 127, 128, 129, 255, 256, 1000, 4097, (1 << 16) + 7, 1 << 20])
+# n % 4 == 0 and runs >= 8192 keys take the TMA-staged merge (ragged run ends -> partial chunks);
+# other sizes exercise the register-window merge
+@pytest.mark.parametrize("n", [0, 1, 2, 31, 127, 128, 129, 255, 256, 1000, 4097, (1 << 16) + 7, 1 << 20,
+                               100004, 3 * (1 << 18) + 12, 40000])
 def test_sizes(g, rt, n):
     keys = synth.keys_int32(n, seed=n).numpy()
     out, st = run_sort(g, rt, keys)
@@ -68,7 +71,7 @@ def test_adversarial(g, rt, kind):
 def test_forest(g):
     import torch
     seg = 1 << 14
-    k = 37
+    k = 37  # total length 37 * 2^14 + 5: register-window merges
     keys = synth.keys_int32(seg * k + 5, seed=3).numpy()
     segments = [(i * seg, (i + 1) * seg) for i in range(k)] + [(seg * k, seg * k + 5)]
     d = torch.from_numpy(keys).cuda()
@@ -96,3 +99,18 @@ def test_full_size_config1(g):
     ref, tasks, inv = oracle.mergesort(keys.numpy(), 128)
     assert np.array_equal(d.cpu().numpy(), ref)
     assert (st.tasks, st.invocations) == (tasks, inv) == (262143, 393214)
+
+
+def test_forest_tma_segments(g):
+    import torch
+    # segment lengths multiple of 4 but not of the 512-key chunk: TMA merges with partial chunks,
+    # neighbouring roots writing adjacent keys concurrently
+    lens = [20004 + 4 * i for i in range(24)]
+    bounds = np.cumsum([0] + lens)
+    keys = synth.keys_int32(int(bounds[-1]), seed=9).numpy()
+    d = torch.from_numpy(keys).cuda()
+    segs = [(int(bounds[i]), int(bounds[i + 1])) for i in range(len(lens))]
+    g.mergesort_forest_(d, segs, grid_size=148, block_size=128, max_tasks_per_worker=1024, watchdog_ns=WD)
+    out = d.cpu().numpy()
+    for l, r in segs:
+        assert np.array_equal(out[l:r], np.sort(keys[l:r]))

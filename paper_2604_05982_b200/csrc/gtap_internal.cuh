@@ -32,13 +32,19 @@ constexpr int kDataWords = 4;  // 16-B payload per record (GTAP_MAX_TASK_DATA_SI
 // function, parent/child IDs, and a resumption state"). 32 B = one L2 sector;
 // two 16-B vector accesses. Child results land in the parent's data[2 + ordinal]
 // (copy-at-finish, R8), so a finished child's record is freed at once.
+// The 8-B head {pending, acc} is one 64-bit atomic word: tables whose
+// continuation only needs the SUM of the child results (fib, "a + b")
+// deliver the result and the join decrement in one relaxed atom.add.u64
+// (kJoinReduceAdd); other tables store into d[2 + ordinal] and decrement
+// `pending` with acq_rel.
 struct __align__(32) TaskRec {
-    uint32_t meta;     // fn:8 | state:8 | ordinal:8 | queue:8
     int32_t pending;   // outstanding children of the current join epoch
-    uint32_t parent;   // parent record id, kNone for roots / no-taskwait tasks
-    uint32_t aux;      // kRootFlag | root index for roots, else 0
+    uint32_t acc;      // sum of child results delivered with the decrement (kJoinReduceAdd)
+    uint32_t meta;     // fn:8 | state:8 | ordinal:8 | queue:8
+    uint32_t parent;   // parent record id; kRootFlag | root index for roots; kNone: no parent
     uint32_t d[kDataWords];
 };
+__host__ __device__ inline bool is_root_link(uint32_t parent) { return parent != 0xFFFFFFFFu && (parent & 0x80000000u); }
 static_assert(sizeof(TaskRec) == 32, "record must be one 32-B sector");
 
 __host__ __device__ inline uint32_t make_meta(uint32_t fn, uint32_t state, uint32_t ord, uint32_t q) {
@@ -217,6 +223,11 @@ __device__ __forceinline__ long long atom_add_acq_rel(long long* p, long long v)
 __device__ __forceinline__ uint32_t atom_add_relaxed(uint32_t* p, uint32_t v) {
     uint32_t o;
     asm volatile("atom.relaxed.gpu.global.add.u32 %0, [%1], %2;" : "=r"(o) : "l"(p), "r"(v) : "memory");
+    return o;
+}
+__device__ __forceinline__ unsigned long long atom_add_relaxed_u64(void* p, unsigned long long v) {
+    unsigned long long o;
+    asm volatile("atom.relaxed.gpu.global.add.u64 %0, [%1], %2;" : "=l"(o) : "l"(p), "l"(v) : "memory");
     return o;
 }
 __device__ __forceinline__ void red_add_release(unsigned long long* p, unsigned long long v) {

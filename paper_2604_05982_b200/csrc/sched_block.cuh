@@ -30,7 +30,7 @@ template <class T>
 struct BlockSmem {
     uint32_t task_id;         // task of this cycle (kNone: none)
     uint32_t exit_flag;
-    uint32_t fn, state, parent, aux, ord;
+    uint32_t fn, state, parent, ord;
     uint32_t d[kDataWords];
     uint32_t nspawn;          // staged children (smem atomic)
     uint32_t action;          // 1 finish, 2 suspend
@@ -152,7 +152,7 @@ __device__ bool block_publish_spawns(const KParams& p, BLeader& L, BlockSmem<T>&
         if (lane < c) {
             const ChildSpec cs = sm.spawns[b + lane];
             TaskRec* r = p.rec + id;
-            st_v4(r, make_uint4(make_meta(cs.fn, 0, b + lane, 0), 0u, parent_id, 0u));
+            st_v4(r, make_uint4(0u, 0u, make_meta(cs.fn, 0, b + lane, 0), parent_id));
             st_v4(&r->d[0], make_uint4(cs.d[0], cs.d[1], cs.d[2], cs.d[3]));
             const uint32_t i = b + lane;
             if (keep_last && i == cnt - 1u) L.kept = id;  // lane-local; broadcast below
@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) block_sched_ker
             const RootSpec rs = p.roots[r];
             const uint32_t id = (w << p.logM) + i;
             TaskRec* rec = p.rec + id;
-            st_v4(rec, make_uint4(make_meta(rs.fn, 0, 0, 0), 0u, kNone, kRootFlag | r));
+            st_v4(rec, make_uint4(0u, 0u, make_meta(rs.fn, 0, 0, 0), kRootFlag | r));
             st_v4(&rec->d[0], make_uint4(rs.d[0], rs.d[1], rs.d[2], rs.d[3]));
             ring[i & qmask] = id;
         }
@@ -292,8 +292,8 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) block_sched_ker
                 if (lane == 0) {
                     const uint4 h = ld_relaxed_v4(p.rec + id);
                     const uint4 dv = ld_relaxed_v4(&p.rec[id].d[0]);
-                    sm.fn = meta_fn(h.x); sm.state = meta_state(h.x); sm.ord = meta_ord(h.x);
-                    sm.parent = h.z; sm.aux = h.w;
+                    sm.fn = meta_fn(h.z); sm.state = meta_state(h.z); sm.ord = meta_ord(h.z);
+                    sm.parent = h.w;
                     sm.d[0] = dv.x; sm.d[1] = dv.y; sm.d[2] = dv.z; sm.d[3] = dv.w;
                     sm.nspawn = 0; sm.action = 0; sm.has_result = 0; sm.err = 0;
                     ++L.st[ST_CYCLES];
@@ -351,7 +351,7 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) block_sched_ker
             if (ok) {
                 if (sm.action == 2) {
                     // suspend: resumption state + join counter
-                    if (lane == 0) st_v2(p.rec + my, make_meta(sm.fn, sm.next_state, sm.ord, 0), total_children);
+                    if (lane == 0) st_v4(p.rec + my, make_uint4(total_children, 0u, make_meta(sm.fn, sm.next_state, sm.ord, 0), sm.parent));
                     if (total_children == 0u) {
                         if (L.kept != kNone) {  // keep the continuation, push the kept child instead
                             if (lane == 0) ring[L.tail & qmask] = L.kept;
@@ -361,16 +361,16 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) block_sched_ker
                     }
                 } else if (fin) {
                     const uint32_t parent = sm.parent;
-                    if (parent != kNone && sm.has_result && lane == 0)
+                    if (parent != kNone && !is_root_link(parent) && sm.has_result && lane == 0)
                         st_relaxed(reinterpret_cast<int32_t*>(&p.rec[parent].d[2 + sm.ord]), sm.result);
                     block_free(p, lane, lane == 0, my);
                     __syncwarp();
                     uint32_t resume = kNone;
                     if (lane == 0) {
-                        if (parent != kNone) {
+                        if (parent != kNone && !is_root_link(parent)) {
                             if (atom_add_acq_rel(&p.rec[parent].pending, -1) == 1) resume = parent;
-                        } else if (sm.aux & kRootFlag) {
-                            p.root_results[sm.aux & ~kRootFlag] = sm.has_result ? (long long)sm.result : 0ll;
+                        } else if (is_root_link(parent)) {
+                            p.root_results[parent & ~kRootFlag] = sm.has_result ? (long long)sm.result : 0ll;
                             if (T::kTaskwait && atom_add_acq_rel(&p.ctl->roots_left, 0xFFFFFFFFu) == 1u)
                                 st_release(&p.ctl->done, 1u);
                         }

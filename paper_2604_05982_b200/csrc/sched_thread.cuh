@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
             const RootSpec rs = p.roots[r];
             const uint32_t id = base_id + i;
             TaskRec* rec = p.rec + id;
-            st_v4(rec, make_uint4(make_meta(rs.fn, 0, 0, 0), 0u, kNone, kRootFlag | r));
+            st_v4(rec, make_uint4(0u, 0u, make_meta(rs.fn, 0, 0, 0), kRootFlag | r));
             st_v4(&rec->d[0], make_uint4(rs.d[0], rs.d[1], rs.d[2], rs.d[3]));
             ring[i & qmask] = id;
         }
@@ -268,18 +268,17 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
         // ================= (2) execute, one task per lane =================
         Out o;
         o.init();
-        uint32_t parent = kNone, aux = 0, ord = 0, myfn = 0;
+        uint32_t parent = kNone, ord = 0, myfn = 0;
         uint32_t mydata[kDataWords] = {0, 0, 0, 0};
         if (my != kNone) {
             const uint4 h = ld_relaxed_v4(p.rec + my);
             const uint4 dv = ld_relaxed_v4(&p.rec[my].d[0]);
             const uint32_t d[kDataWords] = {dv.x, dv.y, dv.z, dv.w};
             if (T::kHasHeavy) { mydata[0] = dv.x; mydata[1] = dv.y; mydata[2] = dv.z; mydata[3] = dv.w; }
-            parent = h.z;
-            aux = h.w;
-            ord = meta_ord(h.x);
-            myfn = meta_fn(h.x);
-            T::exec(args, meta_fn(h.x), meta_state(h.x), d, o, bx);
+            parent = h.w;
+            ord = meta_ord(h.z);
+            myfn = meta_fn(h.z);
+            T::exec(args, meta_fn(h.z), meta_state(h.z), d, o, bx);
             if (o.action == 0u) o.err = GTAP_E_BAD_STATE;
         }
         __syncwarp();
@@ -332,7 +331,7 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
                     const uint32_t g = excl + c;
                     const uint32_t cid = (g < fromF) ? sm.fbuf[g] : sm.abuf[g - fromF];
                     TaskRec* cr = p.rec + cid;
-                    st_v4(cr, make_uint4(make_meta(o.cfn[c], 0, c, 0), 0u, T::kTaskwait ? my : kNone, 0u));
+                    st_v4(cr, make_uint4(0u, 0u, make_meta(o.cfn[c], 0, c, 0), T::kTaskwait ? my : kNone));
                     st_v4(&cr->d[0], make_uint4(o.cd[c][0], o.cd[c][1], o.cd[c][2], o.cd[c][3]));
                     sm.cbuf[g] = cid | (task_is_heavy<T>(o.cfn[c], o.cd[c]) ? kHeavyBit : 0u);
                 }
@@ -341,7 +340,7 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
         // suspend: store the resumption state and the join counter
         uint32_t resume_id = kNone;
         if (o.action == Out::kSuspend) {
-            st_v2(p.rec + my, make_meta(myfn, o.next_state, ord, 0), nc);
+            st_v4(p.rec + my, make_uint4(nc, 0u, make_meta(myfn, o.next_state, ord, 0), parent));
             if (nc == 0u) resume_id = my | (task_is_heavy<T>(myfn, mydata) ? kHeavyBit : 0u);  // empty join
         }
         // surplus freed records go back to their home worker's free ring
@@ -363,17 +362,31 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
             if (lane == 0) st_rfree += __popc(rf);
         }
         // finish: copy the result into the parent's slot (copy-at-finish, R8)
-        if (fin && err == 0u && parent != kNone && o.has_result)
+        if (!T::kJoinReduceAdd && fin && err == 0u && parent != kNone && !is_root_link(parent) && o.has_result)
             st_relaxed(reinterpret_cast<int32_t*>(&p.rec[parent].d[2 + ord]), o.result);
         __syncwarp();
 
         // ================= (3c) join: last child re-enqueues the parent =================
         if (fin && err == 0u) {
-            if (parent != kNone) {
-                const int32_t old = atom_add_acq_rel(&p.rec[parent].pending, -1);
-                if (old == 1) resume_id = parent | (parent_is_heavy<T>(myfn, mydata) ? kHeavyBit : 0u);
-            } else if (aux & kRootFlag) {
-                const uint32_t r = aux & ~kRootFlag;
+            if (parent != kNone && !is_root_link(parent)) {
+                bool last;
+                if constexpr (T::kJoinReduceAdd) {
+                    // one relaxed 64-bit RMW: pending -= 1 and acc += result (the low word never
+                    // underflows, so adding 0xFFFFFFFF carries exactly once into acc: add result - 1)
+                    const unsigned long long inc =
+                        ((unsigned long long)(uint32_t)(o.result - 1) << 32) | 0xFFFFFFFFull;
+                    const unsigned long long old = atom_add_relaxed_u64(&p.rec[parent], inc);
+                    last = (uint32_t)old == 1u;
+                    if (last) {  // the continuation reads the sum as load_result(0) + load_result(1)
+                        const uint32_t sum = (uint32_t)(old >> 32) + (uint32_t)o.result;
+                        st_v2(&p.rec[parent].d[2], sum, 0u);
+                    }
+                } else {
+                    last = atom_add_acq_rel(&p.rec[parent].pending, -1) == 1;
+                }
+                if (last) resume_id = parent | (parent_is_heavy<T>(myfn, mydata) ? kHeavyBit : 0u);
+            } else if (is_root_link(parent)) {
+                const uint32_t r = parent & ~kRootFlag;
                 p.root_results[r] = o.has_result ? (long long)o.result : 0ll;
                 if (T::kTaskwait) {
                     if (atom_add_acq_rel(&p.ctl->roots_left, 0xFFFFFFFFu) == 1u) st_release(&p.ctl->done, 1u);

@@ -19,6 +19,7 @@ struct BfsTable {
     static constexpr int kMaxChildren = 0;  // dynamic (no taskwait: no join metadata)
     static constexpr bool kTaskwait = false;
     static constexpr uint32_t kNumFn = 1;
+    static constexpr bool kJoinReduceAdd = false;  // see TaskRec
     static constexpr int kMaxThreads = 1024, kMinBlocks = 1;  // __launch_bounds__
     static constexpr int kSpawnCap = 1536;
     struct Scratch {

@@ -17,6 +17,7 @@ struct FibTable {
     static constexpr bool kTaskwait = true;
     static constexpr bool kHasHeavy = false;
     static constexpr uint32_t kNumFn = 1;
+    static constexpr bool kJoinReduceAdd = true;  // see TaskRec
     static constexpr int kMaxThreads = 256, kMinBlocks = 4;  // __launch_bounds__
     struct Args {
         uint32_t unused;

@@ -539,6 +539,7 @@ struct MergesortTable {
     static constexpr int kMaxChildren = 2;
     static constexpr bool kTaskwait = true;
     static constexpr uint32_t kNumFn = 1;
+    static constexpr bool kJoinReduceAdd = false;  // see TaskRec
     // placement hint: subtrees whose merges take the TMA path are spread over warps (never two
     // in one warp's kept set, where they would share issue slots and the block's merge slot)
     static constexpr bool kHasHeavy = true;

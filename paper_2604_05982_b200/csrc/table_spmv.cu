@@ -22,6 +22,7 @@ struct SpmvTable {
     static constexpr int kMaxChildren = 32;
     static constexpr bool kTaskwait = false;
     static constexpr uint32_t kNumFn = 1;
+    static constexpr bool kJoinReduceAdd = false;  // see TaskRec
     static constexpr int kMaxThreads = 1024, kMinBlocks = 1;  // __launch_bounds__
     static constexpr int kSpawnCap = 32;
     static constexpr int kMaxHeavy = 256;

@@ -289,9 +289,15 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
         const uint32_t fball = __ballot_sync(0xffffffffu, fin);
         const uint32_t F = __popc(fball);
         if (fin) sm.fbuf[__popc(fball & lt)] = my;
-        uint32_t T_total;
         const uint32_t nc = (err == 0u) ? o.nchild : 0u;
-        const uint32_t excl = warp_excl_scan(nc, lane, T_total);
+        // exclusive prefix of the child counts: one ballot per bit of nc (nc <= MAXC)
+        uint32_t excl = 0, T_total = 0;
+#pragma unroll
+        for (int bit = 0; (1 << bit) <= MAXC; ++bit) {
+            const uint32_t bb = __ballot_sync(0xffffffffu, (nc >> bit) & 1u);
+            excl += (uint32_t)__popc(bb & lt) << bit;
+            T_total += (uint32_t)__popc(bb) << bit;
+        }
         const uint32_t fromF = min(F, T_total);
         uint32_t need = T_total - fromF;
         uint32_t fromRing = 0;
@@ -324,17 +330,18 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
         if (lane == 0) st_tasks += T_total;
 
         // ================= (3b) spawn: write child records =================
-        if (nc) {
+        uint32_t cid[MAXC];
 #pragma unroll
-            for (int c = 0; c < MAXC; ++c) {
-                if ((uint32_t)c < nc) {
-                    const uint32_t g = excl + c;
-                    const uint32_t cid = (g < fromF) ? sm.fbuf[g] : sm.abuf[g - fromF];
-                    TaskRec* cr = p.rec + cid;
-                    st_v4(cr, make_uint4(0u, 0u, make_meta(o.cfn[c], 0, c, 0), T::kTaskwait ? my : kNone));
-                    st_v4(&cr->d[0], make_uint4(o.cd[c][0], o.cd[c][1], o.cd[c][2], o.cd[c][3]));
-                    sm.cbuf[g] = cid | (task_is_heavy<T>(o.cfn[c], o.cd[c]) ? kHeavyBit : 0u);
-                }
+        for (int c = 0; c < MAXC; ++c) {
+            cid[c] = kNone;
+            if ((uint32_t)c < nc) {
+                const uint32_t g = excl + c;
+                cid[c] = (g < fromF) ? sm.fbuf[g] : sm.abuf[g - fromF];
+                TaskRec* cr = p.rec + cid[c];
+                st_v4(cr, make_uint4(0u, 0u, make_meta(o.cfn[c], 0, c, 0), T::kTaskwait ? my : kNone));
+                st_v4(&cr->d[0], make_uint4(o.cd[c][0], o.cd[c][1], o.cd[c][2], o.cd[c][3]));
+                if constexpr (T::kHasHeavy)
+                    sm.cbuf[g] = cid[c] | (task_is_heavy<T>(o.cfn[c], o.cd[c]) ? kHeavyBit : 0u);
             }
         }
         // suspend: store the resumption state and the join counter
@@ -347,18 +354,19 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
         if (F > T_total) {
             const bool mine_free = lane < F - T_total;
             const uint32_t mask = __ballot_sync(0xffffffffu, mine_free);
+            uint32_t fid = 0;
             if (mine_free) {
-                const uint32_t id = sm.fbuf[T_total + lane];
-                const uint32_t home = id >> p.logM;
+                fid = sm.fbuf[T_total + lane];
+                const uint32_t home = fid >> p.logM;
                 const uint32_t grp = __match_any_sync(mask, home);
                 const uint32_t leader = __ffs(grp) - 1u;
                 uint32_t base = 0;
                 if (lane == leader) base = atom_add_relaxed(&p.fm[home].tail, (uint32_t)__popc(grp));
                 base = __shfl_sync(grp, base, leader);
                 const uint32_t slot = base + __popc(grp & lt);
-                st_relaxed(&p.fring[((size_t)home << p.logM) + (slot & mmask)], id + 1u);
+                st_relaxed(&p.fring[((size_t)home << p.logM) + (slot & mmask)], fid + 1u);
             }
-            const uint32_t rf = __ballot_sync(0xffffffffu, mine_free && (sm.fbuf[T_total + lane] >> p.logM) != w);
+            const uint32_t rf = __ballot_sync(0xffffffffu, mine_free && (fid >> p.logM) != w);
             if (lane == 0) st_rfree += __popc(rf);
         }
         // finish: copy the result into the parent's slot (copy-at-finish, R8)
@@ -409,50 +417,74 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
         // ================= (3d) distribute: keep <= 32, push the rest =================
         const uint32_t rball = __ballot_sync(0xffffffffu, resume_id != kNone);
         const uint32_t P = __popc(rball);
-        if (resume_id != kNone) sm.pbuf[__popc(rball & lt)] = resume_id;
-        __syncwarp();
         const uint32_t R = P + T_total;
-        // keep <= 32 runnable tasks (resumed parents first, then children); tasks the table
-        // marks heavy are never kept: they are pushed and published so idle warps take them
         uint32_t keep = 0, pushc = 0, heavy_pushed = 0;
-        for (uint32_t base = 0; base < R; base += 32) {
-            const uint32_t i = base + lane;
-            uint32_t id = kNone;
-            if (i < R) id = (i < P) ? sm.pbuf[i] : sm.cbuf[i - P];
-            const bool hv = (i < R) && (id & kHeavyBit);
-            const uint32_t light = __ballot_sync(0xffffffffu, i < R && !hv);
-            const uint32_t lrank = keep + __popc(light & lt);
-            const bool k = (i < R) && !hv && lrank < 32u;
-            const uint32_t kb = __ballot_sync(0xffffffffu, k);
-            const uint32_t pb = __ballot_sync(0xffffffffu, i < R && !k);
-            if (k) sm.kept[lrank] = id;
-            if (i < R && !k) {
-                const uint32_t slot = tail + pushc + __popc(pb & lt);
-                if (slot - sdone < Q) ring[slot & qmask] = id & ~kHeavyBit;
+        if constexpr (!T::kHasHeavy) {
+            // runnable list = [resumed parents in lane order, children in spawn order]; the first 32
+            // are kept, entry e >= 32 goes to ring slot tail + e - 32: every lane places its own
+            keep = min(R, 32u);
+            pushc = R - keep;
+            if (pushc && tail + pushc - sdone > Q) {
+                if (lane == 0) sdone = ld_relaxed(&mydq->steal_done);
+                sdone = __shfl_sync(0xffffffffu, sdone, 0);
+                if (tail + pushc - sdone > Q) {
+                    if (lane == 0) raise_error(p.ctl, GTAP_E_QUEUE_OVERFLOW);
+                    break;
+                }
             }
-            keep += __popc(kb);
-            pushc += __popc(pb);
-            heavy_pushed |= __ballot_sync(0xffffffffu, hv);
-        }
-        if (pushc && tail + pushc - sdone > Q) {
-            if (lane == 0) sdone = ld_relaxed(&mydq->steal_done);
-            sdone = __shfl_sync(0xffffffffu, sdone, 0);
-            if (tail + pushc - sdone > Q) {
-                if (lane == 0) raise_error(p.ctl, GTAP_E_QUEUE_OVERFLOW);
-                break;
+            if (resume_id != kNone) sm.kept[__popc(rball & lt)] = resume_id;
+#pragma unroll
+            for (int c = 0; c < MAXC; ++c) {
+                if ((uint32_t)c < nc) {
+                    const uint32_t e = P + excl + c;
+                    if (e < 32u) sm.kept[e] = cid[c];
+                    else ring[(tail + (e - 32u)) & qmask] = cid[c];
+                }
             }
-            // capacity was only stale: write the entries skipped above
-            for (uint32_t base = 0, kk = 0, pc = 0; base < R; base += 32) {
+        } else {
+            // keep <= 32 runnable tasks (resumed parents first, then children); tasks the table
+            // marks heavy are never kept: they are pushed and published so idle warps take them
+            if (resume_id != kNone) sm.pbuf[__popc(rball & lt)] = resume_id;
+            __syncwarp();
+            for (uint32_t base = 0; base < R; base += 32) {
                 const uint32_t i = base + lane;
                 uint32_t id = kNone;
                 if (i < R) id = (i < P) ? sm.pbuf[i] : sm.cbuf[i - P];
                 const bool hv = (i < R) && (id & kHeavyBit);
                 const uint32_t light = __ballot_sync(0xffffffffu, i < R && !hv);
-                const bool k = (i < R) && !hv && (kk + __popc(light & lt)) < 32u;
+                const uint32_t lrank = keep + __popc(light & lt);
+                const bool k = (i < R) && !hv && lrank < 32u;
+                const uint32_t kb = __ballot_sync(0xffffffffu, k);
                 const uint32_t pb = __ballot_sync(0xffffffffu, i < R && !k);
-                if (i < R && !k) ring[(tail + pc + __popc(pb & lt)) & qmask] = id & ~kHeavyBit;
-                kk += __popc(__ballot_sync(0xffffffffu, k));
-                pc += __popc(pb);
+                if (k) sm.kept[lrank] = id;
+                if (i < R && !k) {
+                    const uint32_t slot = tail + pushc + __popc(pb & lt);
+                    if (slot - sdone < Q) ring[slot & qmask] = id & ~kHeavyBit;
+                }
+                keep += __popc(kb);
+                pushc += __popc(pb);
+                heavy_pushed |= __ballot_sync(0xffffffffu, hv);
+            }
+            if (pushc && tail + pushc - sdone > Q) {
+                if (lane == 0) sdone = ld_relaxed(&mydq->steal_done);
+                sdone = __shfl_sync(0xffffffffu, sdone, 0);
+                if (tail + pushc - sdone > Q) {
+                    if (lane == 0) raise_error(p.ctl, GTAP_E_QUEUE_OVERFLOW);
+                    break;
+                }
+                // capacity was only stale: write the entries skipped above
+                for (uint32_t base = 0, kk = 0, pc = 0; base < R; base += 32) {
+                    const uint32_t i = base + lane;
+                    uint32_t id = kNone;
+                    if (i < R) id = (i < P) ? sm.pbuf[i] : sm.cbuf[i - P];
+                    const bool hv = (i < R) && (id & kHeavyBit);
+                    const uint32_t light = __ballot_sync(0xffffffffu, i < R && !hv);
+                    const bool k = (i < R) && !hv && (kk + __popc(light & lt)) < 32u;
+                    const uint32_t pb = __ballot_sync(0xffffffffu, i < R && !k);
+                    if (i < R && !k) ring[(tail + pc + __popc(pb & lt)) & qmask] = id & ~kHeavyBit;
+                    kk += __popc(__ballot_sync(0xffffffffu, k));
+                    pc += __popc(pb);
+                }
             }
         }
         __syncwarp();

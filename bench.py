@@ -36,13 +36,13 @@ if ROOT not in sys.path:
 # ---- launch configurations (shared with the full-size parity tests) ----------
 MS_N = 1 << 24
 MS_CUTOFF = 128
-MS_CFG = dict(grid_size=0, block_size=128, max_tasks_per_worker=1024)
+MS_CFG = dict(grid_size=0, block_size=128, max_tasks_per_worker=1024, idle_backoff_ns=32768)
 FIB_N = 40
 FIB_CFG = dict(grid_size=0, block_size=128, max_tasks_per_worker=4096)
 SPMV_ROWS = 1 << 22
 SPMV_NNZ_CUT = 8192
-SPMV_FANOUT = 16
-SPMV_CFG = dict(grid_size=148 * 4, block_size=256, max_tasks_per_worker=1024)
+SPMV_FANOUT = 32
+SPMV_CFG = dict(grid_size=148 * 8, block_size=128, max_tasks_per_worker=1024)
 BFS_SCALE = 22
 BFS_CFG = dict(grid_size=148 * 4, block_size=256, max_tasks_per_worker=1 << 19)
 

@@ -1,0 +1,13 @@
+#!/bin/bash
+# Full evidence pass on one B200: GPU tests, bench JSON, ncu launch list, ncu --set full of the
+# dominant (mergesort) kernel and of fib(40) / SpMV / BFS at their bench sizes.
+cd "$(dirname "$0")/.."
+mkdir -p gpurun_out
+R=${1:-r01}
+./gpu_tests.sh > gpurun_out/${R}_tests.log 2>&1; echo "tests rc=$?"
+tail -3 gpurun_out/${R}_tests.log
+timeout -s KILL 900 python bench.py --steps 5 --warmup 3 > gpurun_out/${R}_bench.json 2> gpurun_out/${R}_bench.err; echo "bench rc=$?"
+timeout -s KILL 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${R}_launches.csv \
+    python bench.py --steps 2 --warmup 1 --no-secondary --no-cpu-baseline > /dev/null 2>&1; echo "launches rc=$?"
+timeout -s KILL 900 ncu --set full --import-source on --clock-control none -k regex:thread_sched -s 1 -c 1 \
+    -o gpurun_out/${R}_prof_ms --force-overwrite python bench_tools/profile_one.py ms 16777216 2 > /dev/null 2>&1; echo "ncu ms rc=$?"

@@ -309,5 +309,38 @@ __device__ __forceinline__ void raise_error(Ctl* ctl, uint32_t code) {
 }
 
 }  // namespace dev
+
+#ifdef GTAP_TRACE
+// Diagnostic task trace (diagnostic builds only, SURVEY.md §5 "tracing"): one record per task
+// invocation {start ns, end ns, worker | state << 24, d0, d1}.
+struct TraceRec {
+    unsigned long long t0, t1;
+    uint32_t who, d0, d1, pad;
+};
+constexpr uint32_t kTraceCap = 1u << 22;
+__device__ TraceRec g_trace[kTraceCap];
+__device__ uint32_t g_trace_n;
+__device__ __forceinline__ void trace_rec(unsigned long long t0, uint32_t who, uint32_t d0, uint32_t d1) {
+    const uint32_t i = atomicAdd(&g_trace_n, 1u);
+    if (i < kTraceCap) {
+        TraceRec r;
+        r.t0 = t0; r.t1 = dev::globaltimer(); r.who = who; r.d0 = d0; r.d1 = d1; r.pad = 0;
+        g_trace[i] = r;
+    }
+}
+// device globals are per translation unit (no -rdc): each table file defines its own reader
+#define GTAP_TRACE_READER(NAME)                                                                        \
+    extern "C" int gtap_trace_read_##NAME(void* host, uint32_t cap, uint32_t* n) {                     \
+        uint32_t cnt = 0;                                                                              \
+        cudaMemcpyFromSymbol(&cnt, gtap::g_trace_n, 4);                                                \
+        *n = cnt;                                                                                      \
+        uint32_t m = cnt < cap ? cnt : cap;                                                            \
+        if (m > gtap::kTraceCap) m = gtap::kTraceCap;                                                  \
+        if (m) cudaMemcpyFromSymbol(host, gtap::g_trace, sizeof(gtap::TraceRec) * m);                  \
+        const uint32_t z = 0;                                                                          \
+        cudaMemcpyToSymbol(gtap::g_trace_n, &z, 4);                                                    \
+        return 0;                                                                                      \
+    }
+#endif
 }  // namespace gtap
 #endif

@@ -378,4 +378,5 @@ gtap_status gtap_finalize(gtap_runtime* rt) {
 
 void gtap_table_destroy(const gtap_task_table* t) { delete const_cast<gtap_task_table*>(t); }
 
+
 }  // extern "C"

@@ -322,11 +322,17 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) block_sched_ker
         if (my == kNone) continue;
 
         // ================= all threads: run the task body =================
+#ifdef GTAP_TRACE
+        const unsigned long long tr0 = dev::globaltimer();
+#endif
         {
             const uint32_t d[kDataWords] = {sm.d[0], sm.d[1], sm.d[2], sm.d[3]};
             T::exec_block(args, ctx, sm.fn, sm.state, d);
         }
         __syncthreads();
+#ifdef GTAP_TRACE
+        if (tid == 0) trace_rec(tr0, w | (sm.state << 24), sm.d[0], sm.d[1]);
+#endif
 
         // ================= warp 0: spawn / join / finish =================
         if (warp == 0) {

@@ -95,3 +95,7 @@ extern "C" gtap_status gtap_bfs_init_depth(int32_t* depth, uint32_t nv, int32_t 
     bfs_init_depth_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(depth, nv, src);
     return cudaGetLastError() == cudaSuccess ? GTAP_OK : GTAP_E_CUDA;
 }
+
+#ifdef GTAP_TRACE
+GTAP_TRACE_READER(bfs)
+#endif

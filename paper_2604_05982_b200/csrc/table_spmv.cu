@@ -44,17 +44,37 @@ struct SpmvTable {
         uint32_t pad;
     };
 
+    // streaming loads for the matrix (read once: do not displace x from L2), read-only path for x
+    __device__ __forceinline__ static int32_t ld_col(const int32_t* p) { return __ldcs(p); }
+    __device__ __forceinline__ static float ld_val(const float* p) { return __ldcs(p); }
+    // 8 lanes per row; each lane keeps 4 independent (col, val, x) loads in flight per iteration
     __device__ __forceinline__ static float row_group8(const Args& a, int32_t s, int32_t e, uint32_t g) {
-        float acc = 0.f;
+        float acc0 = 0.f, acc1 = 0.f;
         int32_t j = s + (int32_t)g;
-        for (; j + 8 < e; j += 16) {
-            const int32_t c0 = __ldg(&a.col[j]), c1 = __ldg(&a.col[j + 8]);
-            const float v0 = __ldg(&a.val[j]), v1 = __ldg(&a.val[j + 8]);
-            acc = fmaf(v0, __ldg(&a.x[c0]), acc);
-            acc = fmaf(v1, __ldg(&a.x[c1]), acc);
+        for (; j + 24 < e; j += 32) {
+            const int32_t c0 = ld_col(&a.col[j]), c1 = ld_col(&a.col[j + 8]);
+            const int32_t c2 = ld_col(&a.col[j + 16]), c3 = ld_col(&a.col[j + 24]);
+            const float v0 = ld_val(&a.val[j]), v1 = ld_val(&a.val[j + 8]);
+            const float v2 = ld_val(&a.val[j + 16]), v3 = ld_val(&a.val[j + 24]);
+            const float x0 = __ldg(&a.x[c0]), x1 = __ldg(&a.x[c1]), x2 = __ldg(&a.x[c2]), x3 = __ldg(&a.x[c3]);
+            acc0 = fmaf(v0, x0, acc0);
+            acc1 = fmaf(v1, x1, acc1);
+            acc0 = fmaf(v2, x2, acc0);
+            acc1 = fmaf(v3, x3, acc1);
         }
-        if (j < e) acc = fmaf(__ldg(&a.val[j]), __ldg(&a.x[__ldg(&a.col[j])]), acc);
-        return acc;
+        // tail: up to 3 more strided elements per lane, loads issued together
+        int32_t c[3];
+        float v[3];
+#pragma unroll
+        for (int u = 0; u < 3; ++u) {
+            const int32_t jj = j + 8 * u;
+            c[u] = jj < e ? ld_col(&a.col[jj]) : 0;
+            v[u] = jj < e ? ld_val(&a.val[jj]) : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < 3; ++u)
+            if (j + 8 * u < e) acc0 = fmaf(v[u], __ldg(&a.x[c[u]]), acc0);
+        return acc0 + acc1;
     }
 
     template <class Ctx>
@@ -82,26 +102,64 @@ struct SpmvTable {
         auto& sc = ctx.sm.scratch;
         if (tid == 0) sc.nheavy = 0;
         __syncthreads();
-        // light rows: 8-lane groups, 4 rows per warp
+        // light rows: 8-lane groups, each group owns 4 consecutive rows at a time; every lane keeps
+        // 4 rows x 2 strided (col, val, x) loads in flight, then the group reduces 4 sums by shuffle
         const uint32_t lane = tid & 31u, g = lane & 7u;
         const uint32_t grp = tid >> 3, ngrp = bd >> 3;
-        for (uint32_t base = lo; base < hi; base += ngrp) {   // uniform trip count
-            const uint32_t row = base + grp;
-            const bool valid = row < hi;
-            int32_t rs = 0, re = 0;
-            if (valid) { rs = __ldg(&a.row_ptr[row]); re = __ldg(&a.row_ptr[row + 1]); }
-            uint32_t queued = 0;
-            if (valid && re - rs > kLight && g == 0) {
-                const uint32_t hidx = atomicAdd(&sc.nheavy, 1u);
-                if (hidx < (uint32_t)kMaxHeavy) { sc.heavy[hidx] = row; queued = 1u; }
+        constexpr uint32_t RPG = 4;
+        for (uint32_t base = lo; base < hi; base += ngrp * RPG) {   // uniform trip count
+            const uint32_t r0 = base + grp * RPG;
+            // row_ptr[r0 .. r0+4] by lanes 0..4 of the group, shared by shuffle
+            int32_t rpv = 0;
+            if (g <= RPG && r0 + g <= hi) rpv = __ldg(&a.row_ptr[r0 + g]);
+            int32_t rs[RPG], re[RPG];
+            bool valid[RPG], queued[RPG];
+#pragma unroll
+            for (uint32_t q = 0; q < RPG; ++q) {
+                rs[q] = __shfl_sync(0xffffffffu, rpv, (lane & ~7u) + q);
+                re[q] = __shfl_sync(0xffffffffu, rpv, (lane & ~7u) + q + 1);
+                valid[q] = r0 + q < hi;
+                uint32_t qd = 0;
+                if (valid[q] && re[q] - rs[q] > kLight && g == 0) {
+                    const uint32_t hidx = atomicAdd(&sc.nheavy, 1u);
+                    if (hidx < (uint32_t)kMaxHeavy) { sc.heavy[hidx] = r0 + q; qd = 1u; }
+                }
+                queued[q] = __shfl_sync(0xffffffffu, qd, lane & ~7u) != 0u;
+                if (!valid[q] || queued[q]) re[q] = rs[q];  // nothing to do for this row here
             }
-            queued = __shfl_sync(0xffffffffu, queued, lane & ~7u);
-            const bool compute = valid && !queued;
-            float acc = compute ? row_group8(a, rs, re, g) : 0.f;
-            acc += __shfl_xor_sync(0xffffffffu, acc, 4);
-            acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-            acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-            if (compute && g == 0) a.y[row] = acc;
+            float acc[RPG] = {0.f, 0.f, 0.f, 0.f};
+            // passes of 16 keys per row (2 per lane); most rows (Pareto, mean ~32) need 1-2 passes
+            int32_t maxlen = 0;
+#pragma unroll
+            for (uint32_t q = 0; q < RPG; ++q) maxlen = max(maxlen, re[q] - rs[q]);
+            for (int32_t off = (int32_t)g; off < maxlen; off += 16) {
+                int32_t c[RPG][2];
+                float v[RPG][2];
+                // branch-free: out-of-row slots load a valid key of the row (or of row_ptr[lo]) and are
+                // multiplied by zero, so every lane issues all 8 (col, val) and 8 x loads back to back
+#pragma unroll
+                for (uint32_t q = 0; q < RPG; ++q)
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        const int32_t j = rs[q] + off + 8 * u;
+                        const bool in = j < re[q];
+                        const int32_t jj = in ? j : s;
+                        c[q][u] = ld_col(&a.col[jj]);
+                        v[q][u] = in ? ld_val(&a.val[jj]) : 0.f;
+                    }
+#pragma unroll
+                for (uint32_t q = 0; q < RPG; ++q)
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) acc[q] = fmaf(v[q][u], __ldg(&a.x[c[q][u]]), acc[q]);
+            }
+#pragma unroll
+            for (uint32_t q = 0; q < RPG; ++q) {
+                float t = acc[q];
+                t += __shfl_xor_sync(0xffffffffu, t, 4);
+                t += __shfl_xor_sync(0xffffffffu, t, 2);
+                t += __shfl_xor_sync(0xffffffffu, t, 1);
+                if (g == q && valid[q] && !queued[q]) a.y[r0 + q] = t;
+            }
         }
         __syncthreads();
         // heavy rows: whole block per row
@@ -113,12 +171,14 @@ struct SpmvTable {
             int32_t j = rs + (int32_t)tid;
             const int32_t st = (int32_t)bd;
             for (; j + 3 * st < re; j += 4 * st) {
-                const int32_t c0 = __ldg(&a.col[j]), c1 = __ldg(&a.col[j + st]);
-                const int32_t c2 = __ldg(&a.col[j + 2 * st]), c3 = __ldg(&a.col[j + 3 * st]);
-                acc0 = fmaf(__ldg(&a.val[j]), __ldg(&a.x[c0]), acc0);
-                acc1 = fmaf(__ldg(&a.val[j + st]), __ldg(&a.x[c1]), acc1);
-                acc2 = fmaf(__ldg(&a.val[j + 2 * st]), __ldg(&a.x[c2]), acc2);
-                acc3 = fmaf(__ldg(&a.val[j + 3 * st]), __ldg(&a.x[c3]), acc3);
+                const int32_t c0 = ld_col(&a.col[j]), c1 = ld_col(&a.col[j + st]);
+                const int32_t c2 = ld_col(&a.col[j + 2 * st]), c3 = ld_col(&a.col[j + 3 * st]);
+                const float v0 = ld_val(&a.val[j]), v1 = ld_val(&a.val[j + st]);
+                const float v2 = ld_val(&a.val[j + 2 * st]), v3 = ld_val(&a.val[j + 3 * st]);
+                acc0 = fmaf(v0, __ldg(&a.x[c0]), acc0);
+                acc1 = fmaf(v1, __ldg(&a.x[c1]), acc1);
+                acc2 = fmaf(v2, __ldg(&a.x[c2]), acc2);
+                acc3 = fmaf(v3, __ldg(&a.x[c3]), acc3);
             }
             for (; j < re; j += st) acc0 = fmaf(__ldg(&a.val[j]), __ldg(&a.x[__ldg(&a.col[j])]), acc0);
             float acc = (acc0 + acc1) + (acc2 + acc3);
@@ -153,3 +213,7 @@ extern "C" const gtap_task_table* gtap_table_spmv(const int32_t* row_ptr, const 
     gtap::SpmvTable::Args a{row_ptr, col, val, x, y, nrows, nnz_cut, fanout, 0u};
     return gtap::make_table<gtap::SpmvTable>("spmv", a, &gtap::validate_spmv);
 }
+
+#ifdef GTAP_TRACE
+GTAP_TRACE_READER(spmv)
+#endif

@@ -44,7 +44,7 @@ SPMV_NNZ_CUT = 8192
 SPMV_FANOUT = 32
 SPMV_CFG = dict(grid_size=148 * 8, block_size=128, max_tasks_per_worker=1024)
 BFS_SCALE = 22
-BFS_CFG = dict(grid_size=148 * 4, block_size=256, max_tasks_per_worker=1 << 19)
+BFS_CFG = dict(grid_size=148 * 4, block_size=256, max_tasks_per_worker=1 << 19, idle_backoff_ns=1024)
 
 L2_FLUSH_BYTES = 256 << 20
 METRIC = "Mkeys/s (mergesort 2^24 int32, cutoff 128), device-timed"
@@ -278,13 +278,17 @@ def bench_atomics(dev):
     return out
 
 
-def bench_spmv(dev, reps=5):
+def bench_spmv(dev, ws=1, rank=0, reps=5):
+    """configs[3]: x replicated, rows partitioned over ranks by nnz, one all_gather of y after timing."""
     import torch
 
     import synth
     import paper_2604_05982_b200 as g
+    from paper_2604_05982_b200 import shard
     rp, col, val, x = synth.powerlaw_csr(SPMV_ROWS, seed=7, device=dev)
-    y = torch.empty(SPMV_ROWS, dtype=torch.float32, device=dev)
+    ranges = shard.split_rows_by_nnz(rp.cpu(), ws)
+    lo, hi = ranges[rank]
+    y = torch.zeros(SPMV_ROWS, dtype=torch.float32, device=dev)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
     rt = g.Runtime(g.GTAP_WORKER_BLOCK, dev.index, **SPMV_CFG)
     ms = []
@@ -292,17 +296,20 @@ def bench_spmv(dev, reps=5):
     for i in range(reps + 1):
         flush.fill_(1)
         rt.reset()
-        y, st = g.spmv(rp, col, val, x, y, SPMV_NNZ_CUT, SPMV_FANOUT, rt=rt)
+        y, st = g.spmv(rp, col, val, x, y, SPMV_NNZ_CUT, SPMV_FANOUT, rows=(lo, hi), rt=rt)
         if i:
             ms.append(st.device_ms)
     rt.close()
-    t = statistics.median(ms)
+    t = _max_over_ranks(statistics.median(ms), ws)
+    if ws > 1:  # the only collective: gather the y slices (outside the timed region)
+        y = shard.gather_slices(y[lo:hi].contiguous(), ranges, rank)
     nnz = int(rp[-1].item())
     algo = 8.0 * nnz + 12.0 * SPMV_ROWS  # col+val per nnz; row_ptr + y + x once per row
     pk, _ = peaks()
-    return dict(workload="SpMV power-law 2^22 rows (configs[3]), block-level", metric="GB/s",
-                value=algo / (t * 1e-3) / 1e9, gflops=2.0 * nnz / (t * 1e-3) / 1e9, ms=t, nnz=nnz,
-                tasks=st.tasks, frac_hbm=algo / (t * 1e-3) / 1e9 / pk["hbm_gbs"], traffic=profile_traffic("spmv"))
+    return dict(workload=f"SpMV power-law 2^22 rows (configs[3]), block-level, rows split over {ws} GPU(s)",
+                metric="GB/s", value=algo / (t * 1e-3) / 1e9, gflops=2.0 * nnz / (t * 1e-3) / 1e9, ms=t, nnz=nnz,
+                tasks=st.tasks, frac_hbm_per_gpu=algo / ws / (t * 1e-3) / 1e9 / pk["hbm_gbs"],
+                traffic=profile_traffic("spmv"), scaling="strong", y_checksum=float(y.double().sum().item()))
 
 
 def bench_bfs(dev, nsrc=4):
@@ -368,11 +375,14 @@ def run_ours(args):
             secondary.append(dict(workload="L2 atomic probes", metric="ops/s", value=atoms))
         except Exception as e:  # secondary results must not kill the main line
             secondary.append(dict(workload="fib40/atomics", error=repr(e)))
-        for fn in (bench_spmv, bench_bfs):
-            try:
-                secondary.append(fn(dev))
-            except Exception as e:
-                secondary.append(dict(workload=fn.__name__, error=repr(e)))
+        try:
+            secondary.append(bench_spmv(dev, ws, rank))
+        except Exception as e:
+            secondary.append(dict(workload="bench_spmv", error=repr(e)))
+        try:
+            secondary.append(bench_bfs(dev))
+        except Exception as e:
+            secondary.append(dict(workload="bench_bfs", error=repr(e)))
     # the only collective: gather per-rank checksums after timing
     if ws > 1:
         import torch.distributed as dist

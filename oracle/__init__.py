@@ -37,6 +37,8 @@ def lib():
         i64p = ctypes.POINTER(ctypes.c_int64)
         vp = ctypes.c_void_p
         L.oracle_fib.argtypes = [ctypes.c_int32, i64p, i64p, i64p]
+        L.oracle_fib_cutoff.argtypes = [ctypes.c_int32, ctypes.c_int32, i64p, i64p, i64p, i64p]
+        L.oracle_fib_cutoff.restype = ctypes.c_int
         L.oracle_mergesort.argtypes = [vp, vp, ctypes.c_int64, ctypes.c_int64, i64p, i64p]
         L.oracle_spmv.argtypes = [vp, vp, vp, vp, ctypes.c_int64, vp, vp]
         L.oracle_bfs.argtypes = [vp, vp, ctypes.c_int64, ctypes.c_int32, vp]
@@ -64,6 +66,15 @@ def fib(n: int):
     if rc != 0:
         raise ValueError(f"fib: n={n} out of range")
     return v.value, c.value, i.value
+
+
+def fib_cutoff(n: int, cutoff: int):
+    """(value, tasks, invocations, serial_calls) of fib with a cutoff."""
+    v, t, i, c = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    rc = lib().oracle_fib_cutoff(n, cutoff, ctypes.byref(v), ctypes.byref(t), ctypes.byref(i), ctypes.byref(c))
+    if rc != 0:
+        raise ValueError(f"fib_cutoff: bad arguments n={n} cutoff={cutoff}")
+    return v.value, t.value, i.value, c.value
 
 
 def mergesort(keys, cutoff: int = 128):

@@ -55,6 +55,42 @@ int oracle_fib(int32_t n, int64_t *value, int64_t *calls, int64_t *invocations)
     return 0;
 }
 
+/*
+ * fib with a cutoff (EPAQ experiment): a task
+ * with n < cutoff runs the serial recursion ("tasks that reach the cutoff
+ * execute additional serial work") and finishes; otherwise it spawns
+ * fib(n-1), fib(n-2), joins and returns a + b. cutoff <= 2 is the no-cutoff
+ * program above. Also counts the serial calls made inside cutoff tasks.
+ */
+static int64_t fib_serial(int32_t n, int64_t *serial_calls)
+{
+    *serial_calls += 1;
+    if (n < 2) return n;
+    return fib_serial(n - 1, serial_calls) + fib_serial(n - 2, serial_calls);
+}
+
+static int64_t fib_cut_rec(int32_t n, int32_t cutoff, int64_t *tasks, int64_t *invocations, int64_t *serial)
+{
+    *tasks += 1;
+    if (n < cutoff || n < 2) {
+        *invocations += 1;
+        return fib_serial(n, serial);
+    }
+    int64_t a = fib_cut_rec(n - 1, cutoff, tasks, invocations, serial);
+    int64_t b = fib_cut_rec(n - 2, cutoff, tasks, invocations, serial);
+    *invocations += 2;
+    return a + b;
+}
+
+int oracle_fib_cutoff(int32_t n, int32_t cutoff, int64_t *value, int64_t *tasks, int64_t *invocations,
+                      int64_t *serial_calls)
+{
+    if (n < 0 || n > 92 || cutoff < 0) return -1;
+    *tasks = *invocations = *serial_calls = 0;
+    *value = fib_cut_rec(n, cutoff, tasks, invocations, serial_calls);
+    return 0;
+}
+
 /* ------------------------------------------------------------ mergesort */
 /*
  * P:153-165 (Prog. cutoff mergesort, §4.4) with the state machine of

@@ -96,6 +96,7 @@ int device_sm_count(int dev) {
 gtap_status geometry(gtap_runtime* rt, const gtap_task_table* t, uint32_t* W, uint32_t* grid, uint32_t* block) {
     if (t->kind != rt->cfg.worker_kind) return GTAP_E_INVAL;
     const uint32_t bs = rt->cfg.block_size;
+    if (bs > t->max_block) return GTAP_E_INVAL;  // beyond the table kernel's __launch_bounds__
     int bps = 0;
     size_t smem = 0;
     if (t->occupancy(t, bs, &bps, &smem) != cudaSuccess) return GTAP_E_CUDA;

@@ -40,11 +40,19 @@ struct BlockSmem {
     uint32_t err;
     ChildSpec spawns[T::kSpawnCap];
     typename T::Scratch scratch;
+    // records of this block's own pool freed here, reused first (no global atomics)
+    uint32_t fstack[256];
+    uint32_t nfree;
+    // the kept child is dispatched from its staged spec (no record reload)
+    ChildSpec kept_spec;
+    uint32_t kept_parent, kept_ord, kept_fresh;
 };
 
 // Leader-side (warp 0) persistent state.
 struct BLeader {
     uint32_t tail, split, sdone, bump, fhead, kept, rng, backoff;
+    uint32_t local_dec;            // finished no-taskwait tasks not yet subtracted from ctl->outstanding
+    unsigned long long S_pref;     // own deque word, loaded at acquire time, used at finalize
     unsigned long long st[ST_COUNT];
 };
 
@@ -82,30 +90,55 @@ struct BCtx {
 
 // warp 0: draw `cnt` (<= 32) record IDs from the own pool into out[] (lane i gets out[i]).
 // Returns false (and raises) on exhaustion.
-__device__ __forceinline__ bool block_alloc(const KParams& p, BLeader& L, uint32_t w, uint32_t lane, uint32_t cnt,
-                                            uint32_t& id_out) {
+template <class SM>
+__device__ __forceinline__ bool block_alloc(const KParams& p, BLeader& L, SM& sm, uint32_t w, uint32_t lane,
+                                            uint32_t cnt, uint32_t& id_out) {
     using namespace dev;
     const uint32_t M = 1u << p.logM, mmask = M - 1u;
+    // 1) this block's shared-memory free stack
+    const uint32_t nf = sm.nfree;
+    const uint32_t fs = min(nf, cnt);
+    if (lane < fs) id_out = sm.fstack[nf - 1u - lane];
+    __syncwarp();
+    if (lane == 0) sm.nfree = nf - fs;
+    if (fs == cnt) { __syncwarp(); return true; }
+    // 2) the own free ring (records freed by other blocks)
     uint32_t* myfring = p.fring + ((size_t)w << p.logM);
+    const uint32_t want = cnt - fs;
     uint32_t e = 0;
-    if (lane < cnt) e = ld_relaxed(&myfring[(L.fhead + lane) & mmask]);
+    if (lane < want) e = ld_relaxed(&myfring[(L.fhead + lane) & mmask]);
     const uint32_t valid = __ballot_sync(0xffffffffu, e != 0u);
-    const uint32_t k = min((uint32_t)(__ffs(~valid) - 1), cnt);
-    if (lane < k) {
-        id_out = e - 1u;
-        st_relaxed(&myfring[(L.fhead + lane) & mmask], 0u);
-    }
+    const uint32_t k = min((uint32_t)(__ffs(~valid) - 1), want);
+    if (lane < k) st_relaxed(&myfring[(L.fhead + lane) & mmask], 0u);
+    const uint32_t src = lane - fs;  // lane fs + i takes ring entry i
+    const uint32_t er = __shfl_sync(0xffffffffu, e, src & 31u);
+    if (lane >= fs && lane < fs + k) id_out = er - 1u;
     L.fhead += k;
-    const uint32_t rest = cnt - k;
+    const uint32_t rest = want - k;
     if (rest) {
         if (L.bump + rest > M) {
             if (lane == 0) raise_error(p.ctl, GTAP_E_POOL_EXHAUSTED);
             return false;
         }
-        if (lane >= k && lane < cnt) id_out = (w << p.logM) + L.bump + (lane - k);
+        if (lane >= fs + k && lane < cnt) id_out = (w << p.logM) + L.bump + (lane - fs - k);
         L.bump += rest;
     }
+    __syncwarp();
     return true;
+}
+
+// warp 0, lane 0: free one record -- to the block's smem stack when it is ours, else to its
+// home block's free ring.
+template <class SM>
+__device__ __forceinline__ void block_free1(const KParams& p, SM& sm, uint32_t w, uint32_t id) {
+    using namespace dev;
+    if ((id >> p.logM) == w && sm.nfree < 256u) {
+        sm.fstack[sm.nfree++] = id;
+        return;
+    }
+    const uint32_t home = id >> p.logM;
+    const uint32_t slot = atom_add_relaxed(&p.fm[home].tail, 1u);
+    st_relaxed(&p.fring[((size_t)home << p.logM) + (slot & ((1u << p.logM) - 1u))], id + 1u);
 }
 
 // warp 0: free record `id` (lane-predicated `doit`) to its home free ring.
@@ -133,8 +166,9 @@ __device__ bool block_publish_spawns(const KParams& p, BLeader& L, BlockSmem<T>&
     uint32_t* ring = p.ring + (size_t)w * Q;
     if (cnt == 0) return true;
     if (!T::kTaskwait && count_outstanding) {
-        // outstanding += children before any of them can be published (termination, R6)
-        if (lane == 0) atom_add_acq_rel(&p.ctl->outstanding, (long long)cnt);
+        // outstanding += children before any of them can be published (termination, R6); the
+        // publication's release orders this relaxed add before any thief can run a child
+        if (lane == 0) red_add_relaxed(reinterpret_cast<unsigned long long*>(&p.ctl->outstanding), cnt);
     }
     uint32_t pushc = keep_last ? cnt - 1u : cnt;
     if (pushc && L.tail + pushc - L.sdone > Q) {
@@ -148,15 +182,22 @@ __device__ bool block_publish_spawns(const KParams& p, BLeader& L, BlockSmem<T>&
     for (uint32_t b = 0; b < cnt; b += 32) {
         const uint32_t c = min(32u, cnt - b);
         uint32_t id = kNone;
-        if (!block_alloc(p, L, w, lane, c, id)) return false;
+        if (!block_alloc(p, L, sm, w, lane, c, id)) return false;
         if (lane < c) {
             const ChildSpec cs = sm.spawns[b + lane];
             TaskRec* r = p.rec + id;
             st_v4(r, make_uint4(0u, 0u, make_meta(cs.fn, 0, b + lane, 0), parent_id));
             st_v4(&r->d[0], make_uint4(cs.d[0], cs.d[1], cs.d[2], cs.d[3]));
             const uint32_t i = b + lane;
-            if (keep_last && i == cnt - 1u) L.kept = id;  // lane-local; broadcast below
-            else ring[(L.tail + i) & p.qmask] = id;
+            if (keep_last && i == cnt - 1u) {  // lane-local; broadcast below
+                L.kept = id;
+                sm.kept_spec = cs;
+                sm.kept_parent = parent_id;
+                sm.kept_ord = i;
+                sm.kept_fresh = 1u;
+            } else {
+                ring[(L.tail + i) & p.qmask] = id;
+            }
         }
         if (keep_last && cnt - 1u >= b && cnt - 1u < b + c) {
             L.kept = __shfl_sync(0xffffffffu, L.kept, (cnt - 1u) - b);
@@ -168,10 +209,11 @@ __device__ bool block_publish_spawns(const KParams& p, BLeader& L, BlockSmem<T>&
 }
 
 // warp 0: publish half of the private part if thieves drained the public part.
-__device__ __forceinline__ void block_maybe_publish(const KParams& p, BLeader& L, uint32_t w, uint32_t lane) {
+__device__ __forceinline__ void block_maybe_publish(const KParams& p, BLeader& L, uint32_t w, uint32_t lane,
+                                                    bool use_pref = false) {
     using namespace dev;
     if (lane == 0) {
-        const unsigned long long s = ld_relaxed(&p.dq[w].S);
+        const unsigned long long s = use_pref ? L.S_pref : ld_relaxed(&p.dq[w].S);
         const uint32_t priv = L.tail - L.split;
         if ((uint32_t)s == L.split && priv >= 2u) {
             const uint32_t k = priv >> 1;
@@ -198,6 +240,8 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) block_sched_ker
 
     if (warp == 0) {
         L.tail = L.split = L.sdone = L.bump = L.fhead = 0;
+        L.local_dec = 0;
+        L.S_pref = 0;
         L.kept = kNone;
         L.backoff = 64;
         L.rng = hash32(p.seed * 0x9E3779B97F4A7C15ull + (unsigned long long)w * 32u + lane);
@@ -223,15 +267,18 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) block_sched_ker
         if (lane == 0) L.st[ST_TASKS] += mine;
         __syncwarp();
     }
-    if (tid == 0) { sm.exit_flag = 0; }
+    if (tid == 0) { sm.exit_flag = 0; sm.nfree = 0; sm.kept_fresh = 0; }
+    __syncthreads();
 
     while (true) {
         // ================= warp 0: acquire one task =================
         if (warp == 0) {
             uint32_t id = kNone;
+            bool from_spec = false;
             if (L.kept != kNone) {
                 id = L.kept;
                 L.kept = kNone;
+                from_spec = sm.kept_fresh != 0u;
                 if (lane == 0) ++L.st[ST_KEPT];
             } else if (L.tail != L.split) {  // LIFO pop, private part
                 L.tail -= 1u;
@@ -290,11 +337,19 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) block_sched_ker
             }
             if (id != kNone) {
                 if (lane == 0) {
-                    const uint4 h = ld_relaxed_v4(p.rec + id);
-                    const uint4 dv = ld_relaxed_v4(&p.rec[id].d[0]);
-                    sm.fn = meta_fn(h.z); sm.state = meta_state(h.z); sm.ord = meta_ord(h.z);
-                    sm.parent = h.w;
-                    sm.d[0] = dv.x; sm.d[1] = dv.y; sm.d[2] = dv.z; sm.d[3] = dv.w;
+                    L.S_pref = ld_relaxed(&mydq->S);  // consumed at finalize (publication check)
+                    if (from_spec) {  // a child this block just spawned: its record is not re-read
+                        const ChildSpec cs = sm.kept_spec;
+                        sm.fn = cs.fn; sm.state = 0; sm.ord = sm.kept_ord; sm.parent = sm.kept_parent;
+                        sm.d[0] = cs.d[0]; sm.d[1] = cs.d[1]; sm.d[2] = cs.d[2]; sm.d[3] = cs.d[3];
+                    } else {
+                        const uint4 h = ld_relaxed_v4(p.rec + id);
+                        const uint4 dv = ld_relaxed_v4(&p.rec[id].d[0]);
+                        sm.fn = meta_fn(h.z); sm.state = meta_state(h.z); sm.ord = meta_ord(h.z);
+                        sm.parent = h.w;
+                        sm.d[0] = dv.x; sm.d[1] = dv.y; sm.d[2] = dv.z; sm.d[3] = dv.w;
+                    }
+                    sm.kept_fresh = 0;
                     sm.nspawn = 0; sm.action = 0; sm.has_result = 0; sm.err = 0;
                     ++L.st[ST_CYCLES];
                     ++L.st[ST_INVOC];
@@ -304,6 +359,11 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) block_sched_ker
                 if (lane == 0) ++L.st[ST_IDLE];
                 uint32_t d = 0;
                 if (lane == 0) {
+                    if (!T::kTaskwait && L.local_dec) {  // flush deferred finishes (termination, R6)
+                        const long long dec = (long long)L.local_dec;
+                        L.local_dec = 0;
+                        if (atom_add_acq_rel(&p.ctl->outstanding, -dec) == dec) st_release(&p.ctl->done, 1u);
+                    }
                     d = ld_relaxed(&p.ctl->done);
                     if (!d && p.watchdog_ns && globaltimer() - t0 > p.watchdog_ns) raise_error(p.ctl, GTAP_E_TIMEOUT);
                 }
@@ -343,11 +403,20 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) block_sched_ker
             const bool fin = (sm.action == 1);
             const uint32_t total_children = staged;
             if (ok && !T::kTaskwait && lane == 0) {
-                // one atomic per task: +children (before they are published) -1 for this task (R6)
-                const long long delta = (long long)staged - 1ll;
-                if (delta != 0) {
-                    const long long old = atom_add_acq_rel(&p.ctl->outstanding, delta);
-                    if (old + delta == 0) st_release(&p.ctl->done, 1u);
+                // +children must reach the counter before they are published; this task's -1 may be
+                // deferred (the counter then only stays positive longer): fold it into the +children
+                // when there are children, else batch it locally (flushed every 64 tasks or when idle)
+                if (staged) {
+                    const long long delta = (long long)staged - 1ll - (long long)L.local_dec;
+                    L.local_dec = 0;
+                    if (delta > 0) red_add_relaxed(reinterpret_cast<unsigned long long*>(&p.ctl->outstanding),
+                                                   (unsigned long long)delta);
+                    else if (delta < 0 && atom_add_acq_rel(&p.ctl->outstanding, delta) == -delta)
+                        st_release(&p.ctl->done, 1u);
+                } else if (++L.local_dec >= 64u) {
+                    const long long dec = (long long)L.local_dec;
+                    L.local_dec = 0;
+                    if (atom_add_acq_rel(&p.ctl->outstanding, -dec) == dec) st_release(&p.ctl->done, 1u);
                 }
             }
             if (ok) {
@@ -364,12 +433,13 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) block_sched_ker
                             L.tail += 1u;
                         }
                         L.kept = my;
+                        if (lane == 0) sm.kept_fresh = 0u;  // a continuation: reload its record
                     }
                 } else if (fin) {
                     const uint32_t parent = sm.parent;
                     if (parent != kNone && !is_root_link(parent) && sm.has_result && lane == 0)
                         st_relaxed(reinterpret_cast<int32_t*>(&p.rec[parent].d[2 + sm.ord]), sm.result);
-                    block_free(p, lane, lane == 0, my);
+                    if (lane == 0) block_free1(p, sm, w, my);
                     __syncwarp();
                     uint32_t resume = kNone;
                     if (lane == 0) {
@@ -388,9 +458,10 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) block_sched_ker
                             L.tail += 1u;
                         }
                         L.kept = resume;
+                        if (lane == 0) sm.kept_fresh = 0u;
                     }
                 }
-                block_maybe_publish(p, L, w, lane);
+                block_maybe_publish(p, L, w, lane, true);
             }
             __syncwarp();
         }

@@ -15,6 +15,7 @@ struct gtap_task_table {
     uint32_t taskwait;      // table ever suspends (otherwise GTAP_ASSUME_NO_TASKWAIT semantics)
     uint32_t max_children;  // compile-time bound of the table (GTAP_MAX_CHILD_TASKS)
     uint32_t nfn;           // number of task functions
+    uint32_t max_block;     // __launch_bounds__ max threads of the table's kernel
     const char* name;
     cudaError_t (*launch)(const gtap_task_table*, const gtap::KParams&, uint32_t grid, uint32_t block,
                           cudaStream_t);
@@ -79,6 +80,7 @@ gtap_task_table* make_table(const char* name, const typename T::Args& a,
     t->taskwait = T::kTaskwait ? 1u : 0u;
     t->max_children = (uint32_t)T::kMaxChildren;
     t->nfn = T::kNumFn;
+    t->max_block = (uint32_t)T::kMaxThreads;
     t->name = name;
     if constexpr (T::kKind == GTAP_WORKER_THREAD) {
         t->launch = &launch_thread<T>;

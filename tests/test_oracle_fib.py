@@ -117,3 +117,45 @@ def test_fib3_join_loads():
 def test_range_checked():
     with pytest.raises(ValueError):
         oracle.fib(-1)
+
+
+# ---- fib with cutoff (EPAQ benchmark) ----
+
+def _fib_cut_tasks(n, c):
+    """Task count by an explicit work list (no recursion): a task n >= max(c, 2) has two children."""
+    tasks, work = 0, [n]
+    while work:
+        m = work.pop()
+        tasks += 1
+        if m >= c and m >= 2:
+            work += [m - 1, m - 2]
+    return tasks
+
+
+@pytest.mark.parametrize("n", range(0, 25))
+@pytest.mark.parametrize("c", [0, 1, 2, 3, 5, 10])
+def test_fib_cutoff(n, c):
+    v, tasks, inv, serial = oracle.fib_cutoff(n, c)
+    assert v == fib_iter(n)
+    assert tasks == _fib_cut_tasks(n, c)
+    # every non-leaf task runs 2 invocations, every leaf 1
+    internal = (tasks - 1) // 2
+    assert inv == 2 * internal + (tasks - internal)
+    # serial work: each cutoff task m does 2F(m+1)-1 serial calls of the naive recursion
+    if c <= 2:
+        assert (tasks, inv) == oracle.fib(n)[1:]  # cutoff <= 2 is the no-cutoff program
+
+
+def test_fib_cutoff_serial_calls_closed_form():
+    n, c = 20, 10
+    _, tasks, _, serial = oracle.fib_cutoff(n, c)
+    # leaves of the task tree are fib(9) and fib(8) tasks; count them by explicit expansion
+    leaves = {}
+    work = [n]
+    while work:
+        m = work.pop()
+        if m >= c:
+            work += [m - 1, m - 2]
+        else:
+            leaves[m] = leaves.get(m, 0) + 1
+    assert serial == sum(k * (2 * fib_iter(m + 1) - 1) for m, k in leaves.items())

@@ -260,6 +260,24 @@ def bench_fib(dev, reps=3):
                 join_atomics=tasks - 1)
 
 
+def bench_epaq(dev, cutoff=10, reps=3):
+    """SURVEY §8(f) NEXT #1: fib(40) with cutoff 10, 1 queue vs EPAQ with 3 queues (P:788-789)."""
+    import paper_2604_05982_b200 as g
+    out = {}
+    for nq in (1, 3):
+        with g.Runtime(g.GTAP_WORKER_THREAD, dev.index, num_queues=3, **FIB_CFG) as rt:
+            ms = []
+            for i in range(reps + 1):
+                v, st = g.fib_cutoff(FIB_N, cutoff, nq, rt=rt)
+                assert v == 102334155
+                if i:
+                    ms.append(st.device_ms)
+        out[nq] = (statistics.median(ms), st.tasks)
+    return dict(workload=f"fib(40) cutoff {cutoff}: EPAQ 3 queues vs 1 queue (NEXT #1)", metric="speedup",
+                value=out[1][0] / out[3][0], ms_1q=out[1][0], ms_3q=out[3][0], tasks=out[3][1],
+                paper="~1.8x on GH200 (P:788)")
+
+
 def bench_atomics(dev):
     import torch
 
@@ -373,6 +391,7 @@ def run_ours(args):
                                                 "distinct L2-resident sectors)")
             secondary.append(fibr)
             secondary.append(dict(workload="L2 atomic probes", metric="ops/s", value=atoms))
+            secondary.append(bench_epaq(dev))
         except Exception as e:  # secondary results must not kill the main line
             secondary.append(dict(workload="fib40/atomics", error=repr(e)))
         try:

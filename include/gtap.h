@@ -71,7 +71,8 @@ typedef struct {
                                       records per worker pool, power of two; 0 = 4096 */
     uint32_t queue_capacity;       /* ring slots per deque, power of two; 0 = max_tasks_per_worker */
     uint32_t max_child_tasks;      /* GTAP_MAX_CHILD_TASKS; 0 = table's own bound */
-    uint32_t num_queues;           /* GTAP_NUM_QUEUES (EPAQ); 1 in this build */
+    uint32_t num_queues;           /* GTAP_NUM_QUEUES (EPAQ): deques per warp, 1..8;
+                                      block-level workers: 1; 0 = 1 */
     uint32_t max_task_data_size;   /* GTAP_MAX_TASK_DATA_SIZE bytes; 0 = 16 */
     uint32_t assume_no_taskwait;   /* GTAP_ASSUME_NO_TASKWAIT; informative:
                                       tables that never join set it themselves */
@@ -173,6 +174,13 @@ void gtap_table_destroy(const gtap_task_table *t);
 /* fib (P:1023-1033 + transformed P:1160-1190), thread-level, no cutoff.
  * fn 0, root args {int32 n}, 0 <= n <= 46; result int64 fib(n). */
 const gtap_task_table *gtap_table_fib(void);
+
+/* fib with a cutoff (the EPAQ experiment), thread-level:
+ * n < cutoff runs the serial recursion inside the task. num_queues = 1 (no
+ * EPAQ) or 3 (EPAQ: non-cutoff children -> queue 0, cutoff children ->
+ * queue 1, continuations -> queue 2; needs config.num_queues >= 3). fn 0, root
+ * args {int32 n}, 0 <= n <= 46; result int64 fib(n). NULL on bad arguments. */
+const gtap_task_table *gtap_table_fib_cutoff(int32_t cutoff, uint32_t num_queues);
 
 /* mergesort with cutoff (state machine P:59-74), thread-level.
  * keys: int32[n] device buffer sorted in place; scratch: int32[n] device

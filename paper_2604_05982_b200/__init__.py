@@ -17,7 +17,7 @@ from . import gtap
 from .gtap import (GTAP_WORKER_BLOCK, GTAP_WORKER_THREAD, GtapError, Runtime, RunStats, Table,
                    bfs_init_depth, ubench_atomics)
 
-__all__ = ["gtap", "Runtime", "Table", "RunStats", "GtapError", "fib", "mergesort_", "mergesort_forest_",
+__all__ = ["gtap", "Runtime", "Table", "RunStats", "GtapError", "fib", "fib_cutoff", "mergesort_", "mergesort_forest_",
            "spmv", "bfs", "ubench_atomics", "GTAP_WORKER_THREAD", "GTAP_WORKER_BLOCK"]
 
 
@@ -31,6 +31,23 @@ def fib(n: int, rt: Runtime | None = None, device: int = 0, stream=None, **cfg):
     """fib(n) as the paper's no-cutoff task program on thread-level workers."""
     rt, own = _runtime(GTAP_WORKER_THREAD, rt, device, cfg)
     table = Table.fib()
+    try:
+        rt.spawn_root(table, (n,))
+        rt.run(stream)
+        st = rt.sync()
+        return rt.root_result(0), st
+    finally:
+        table.close()
+        if own:
+            rt.close()
+
+
+def fib_cutoff(n: int, cutoff: int, num_queues: int = 1, rt: Runtime | None = None, device: int = 0, stream=None,
+               **cfg):
+    """fib(n) with a cutoff; num_queues=3 enables EPAQ with the paper's classifier."""
+    cfg.setdefault("num_queues", num_queues)
+    rt, own = _runtime(GTAP_WORKER_THREAD, rt, device, cfg)
+    table = Table.fib_cutoff(cutoff, num_queues)
     try:
         rt.spawn_root(table, (n,))
         rt.run(stream)

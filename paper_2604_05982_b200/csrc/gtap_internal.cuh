@@ -108,11 +108,13 @@ struct KParams {
     uint32_t nroots;
     uint32_t max_child;      // GTAP_MAX_CHILD_TASKS (runtime check)
     uint32_t idle_backoff;   // max idle nanosleep (ns)
+    uint32_t nq;             // deques per worker in the workspace (GTAP_NUM_QUEUES, EPAQ)
+    uint32_t pad2;
     unsigned long long seed;
     unsigned long long watchdog_ns;
     TaskRec* rec;            // W << logM records
-    uint32_t* ring;          // W * (qmask+1)
-    DequeMeta* dq;           // W
+    uint32_t* ring;          // W * nq * (qmask+1)
+    DequeMeta* dq;           // W * nq
     uint32_t* fring;         // W << logM
     FreeMeta* fm;            // W
     Ctl* ctl;
@@ -123,22 +125,22 @@ struct KParams {
 // Host-side layout of the workspace (offsets in bytes).
 struct Layout {
     size_t rec, ring, dq, fring, fm, ctl, roots, results, total;
-    uint32_t W, M, Q, max_roots;
+    uint32_t W, M, Q, max_roots, NQ;
 };
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-inline Layout make_layout(uint32_t W, uint32_t M, uint32_t Q, uint32_t max_roots) {
+inline Layout make_layout(uint32_t W, uint32_t M, uint32_t Q, uint32_t max_roots, uint32_t NQ = 1) {
     Layout L{};
-    L.W = W; L.M = M; L.Q = Q; L.max_roots = max_roots;
+    L.W = W; L.M = M; L.Q = Q; L.max_roots = max_roots; L.NQ = NQ;
     size_t o = 0;
     L.ctl = o;     o = align_up(o + sizeof(Ctl), 256);
-    L.dq = o;      o = align_up(o + sizeof(DequeMeta) * (size_t)W, 256);
+    L.dq = o;      o = align_up(o + sizeof(DequeMeta) * (size_t)W * NQ, 256);
     L.fm = o;      o = align_up(o + sizeof(FreeMeta) * (size_t)W, 256);
     L.roots = o;   o = align_up(o + sizeof(RootSpec) * (size_t)max_roots, 256);
     L.results = o; o = align_up(o + sizeof(long long) * (size_t)max_roots, 256);
     L.fring = o;   o = align_up(o + sizeof(uint32_t) * (size_t)W * M, 256);
-    L.ring = o;    o = align_up(o + sizeof(uint32_t) * (size_t)W * Q, 256);
+    L.ring = o;    o = align_up(o + sizeof(uint32_t) * (size_t)W * NQ * Q, 256);
     L.rec = o;     o = align_up(o + sizeof(TaskRec) * (size_t)W * M, 256);
     L.total = o;
     return L;

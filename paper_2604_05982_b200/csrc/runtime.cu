@@ -63,7 +63,8 @@ gtap_status resolve(const gtap_config* in, gtap_config* c, int sm_count) {
     if (c->queue_capacity == 0) c->queue_capacity = c->max_tasks_per_worker;
     if (!is_pow2(c->queue_capacity) || c->queue_capacity < 64 || c->queue_capacity > (1u << 24)) return GTAP_E_INVAL;
     if (c->num_queues == 0) c->num_queues = 1;
-    if (c->num_queues != 1) return GTAP_E_UNSUPPORTED;  // EPAQ: SURVEY §8(f) NEXT #1
+    if (c->num_queues > 8) return GTAP_E_INVAL;
+    if (c->worker_kind == GTAP_WORKER_BLOCK && c->num_queues != 1) return GTAP_E_INVAL;  // EPAQ: thread-level
     if (c->max_task_data_size == 0) c->max_task_data_size = 16;
     if (c->max_task_data_size > 16) return GTAP_E_UNSUPPORTED;
     if (c->steal_attempts == 0) c->steal_attempts = 4;
@@ -97,6 +98,7 @@ gtap_status geometry(gtap_runtime* rt, const gtap_task_table* t, uint32_t* W, ui
     if (t->kind != rt->cfg.worker_kind) return GTAP_E_INVAL;
     const uint32_t bs = rt->cfg.block_size;
     if (bs > t->max_block) return GTAP_E_INVAL;  // beyond the table kernel's __launch_bounds__
+    if (t->num_queues > rt->cfg.num_queues) return GTAP_E_INVAL;  // EPAQ table needs its queues
     int bps = 0;
     size_t smem = 0;
     if (t->occupancy(t, bs, &bps, &smem) != cudaSuccess) return GTAP_E_CUDA;
@@ -166,7 +168,7 @@ size_t gtap_workspace_bytes(const gtap_config* in) {
     const int sm = in ? device_sm_count(in->device) : 0;
     if (resolve(in, &c, sm > 0 ? sm : 148) != GTAP_OK) return 0;
     const uint32_t W = workers_alloc(c, sm > 0 ? sm : 148);
-    return gtap::make_layout(W, c.max_tasks_per_worker, c.queue_capacity, c.max_roots).total;
+    return gtap::make_layout(W, c.max_tasks_per_worker, c.queue_capacity, c.max_roots, c.num_queues).total;
 }
 
 gtap_status gtap_init(const gtap_config* in, void* d_workspace, size_t bytes, gtap_runtime** out) {
@@ -194,7 +196,7 @@ gtap_status gtap_init(const gtap_config* in, void* d_workspace, size_t bytes, gt
     rt->M = c.max_tasks_per_worker;
     rt->Q = c.queue_capacity;
     rt->max_roots = c.max_roots;
-    rt->L = gtap::make_layout(rt->W_alloc, rt->M, rt->Q, rt->max_roots);
+    rt->L = gtap::make_layout(rt->W_alloc, rt->M, rt->Q, rt->max_roots, c.num_queues);
     if (d_workspace) {
         if (bytes < rt->L.total || ((uintptr_t)d_workspace & 255u)) { delete rt; return GTAP_E_INVAL; }
         rt->ws = static_cast<char*>(d_workspace);
@@ -292,6 +294,7 @@ gtap_status gtap_run(gtap_runtime* rt, void* stream) {
     p.seed = rt->cfg.seed;
     p.watchdog_ns = rt->cfg.watchdog_ns;
     p.idle_backoff = rt->cfg.idle_backoff_ns;
+    p.nq = rt->cfg.num_queues;
     p.rec = reinterpret_cast<gtap::TaskRec*>(rt->ws + rt->L.rec);
     p.ring = reinterpret_cast<uint32_t*>(rt->ws + rt->L.ring);
     p.dq = reinterpret_cast<gtap::DequeMeta*>(rt->ws + rt->L.dq);

@@ -1,5 +1,6 @@
 // sched_thread.cuh -- thread-level persistent scheduler ("thread-executed"
-// mode, §4.1; queue design §4.3.2).
+// mode, §4.1; queue design §4.3.2; EPAQ §4.4
+// P:146-178).
 //
 // One worker = one warp. Each persistent-kernel cycle a warp
 //   (1) acquires up to 32 runnable task IDs: the set kept from its previous
@@ -13,17 +14,27 @@
 //       publishes part of its private deque when thieves have drained the
 //       public part.
 //
-// Deque (B200 design): a power-of-two ring per warp in HBM
-// with a packed 64-bit word S = head | split << 32. The owner pushes and pops
-// at the tail of the PRIVATE part [split, tail) with no atomics at all (tail
-// and split live in registers -- only the owner moves them).
-// Thieves CAS S to claim [head, head + c) of the PUBLIC part [head, split)
-// under a per-victim try-lock; the owner publishes the oldest
-// half of its private part with one red.release when it sees the public part
-// empty, and reclaims from the public part by CAS only when its private part
-// and kept set are empty. This keeps the paper's batched claim-by-CAS for
-// steals but moves the owner's common-case pop off the shared counter
-// whose contention the paper identifies as its scaling limit.
+// Deque (B200 design): a power-of-two ring per warp and
+// queue in HBM with a packed 64-bit word S = head | split << 32. The owner
+// pushes and pops at the tail of the PRIVATE part [split, tail) with no
+// atomics at all (tail and split live in registers -- only the owner moves
+// them). Thieves CAS S to claim [head, head + c) of the PUBLIC part
+// [head, split) under a per-victim try-lock; the owner
+// publishes the oldest half of its private part with one red.release when it
+// sees the public part empty, and reclaims from the public part by CAS only
+// when its private part and kept set are empty. This keeps the paper's
+// batched claim-by-CAS for steals but moves the owner's common-case
+// pop off the shared counter whose contention the paper identifies as its
+// scaling limit.
+//
+// EPAQ (NQ = T::kNumQueues > 1): every warp owns NQ such deques.
+// A child's queue is chosen at spawn (queue(expr)) and a
+// continuation's at taskwait; the suspended parent keeps that
+// index in the top byte of its join word, so the last child learns it from
+// the atomic's return value. Acquisition goes round-robin over the queues
+// starting from the one used last, thieves probe the victims'
+// queues the same way, and the kept set holds ONE queue class (the next one in
+// the rotation), so a warp runs tasks of one execution path per cycle.
 #pragma once
 #include "gtap.h"
 #include "gtap_internal.cuh"
@@ -37,27 +48,38 @@ struct TOut {
     uint32_t action;      // 0 = none, 1 = finish, 2 = suspend
     uint32_t nchild;
     uint32_t next_state;
+    uint32_t next_queue;  // taskwait queue(expr) (EPAQ)
     uint32_t has_result;
     int32_t result;
     uint32_t err;
     uint32_t cfn[MAXC];
+    uint32_t cq[MAXC];    // spawn queue(expr) (EPAQ)
     uint32_t cd[MAXC][kDataWords];
     static constexpr uint32_t kFinish = 1, kSuspend = 2;
-    __device__ __forceinline__ void init() { action = 0; nchild = 0; has_result = 0; err = 0; result = 0; next_state = 0; }
-    // spawn child #i (i is a compile-time constant after inlining)
-    __device__ __forceinline__ void spawn(int i, uint32_t fn, uint32_t d0, uint32_t d1 = 0, uint32_t d2 = 0,
-                                          uint32_t d3 = 0) {
+    __device__ __forceinline__ void init() {
+        action = 0; nchild = 0; has_result = 0; err = 0; result = 0; next_state = 0; next_queue = 0;
+    }
+    // spawn child #i (i is a compile-time constant after inlining) into queue q
+    __device__ __forceinline__ void spawn_q(int i, uint32_t q, uint32_t fn, uint32_t d0, uint32_t d1 = 0,
+                                            uint32_t d2 = 0, uint32_t d3 = 0) {
         if (i >= MAXC) { err = GTAP_E_CHILD_LIMIT; return; }
-        cfn[i] = fn; cd[i][0] = d0; cd[i][1] = d1; cd[i][2] = d2; cd[i][3] = d3;
+        cfn[i] = fn; cq[i] = q; cd[i][0] = d0; cd[i][1] = d1; cd[i][2] = d2; cd[i][3] = d3;
         nchild = (uint32_t)i + 1 > nchild ? (uint32_t)i + 1 : nchild;
     }
-    __device__ __forceinline__ void suspend(uint32_t next) { action = kSuspend; next_state = next; }
+    __device__ __forceinline__ void spawn(int i, uint32_t fn, uint32_t d0, uint32_t d1 = 0, uint32_t d2 = 0,
+                                          uint32_t d3 = 0) {
+        spawn_q(i, 0u, fn, d0, d1, d2, d3);
+    }
+    __device__ __forceinline__ void suspend(uint32_t next, uint32_t q = 0) {
+        action = kSuspend; next_state = next; next_queue = q;
+    }
     __device__ __forceinline__ void finish(int32_t r) { action = kFinish; has_result = 1; result = r; }
     __device__ __forceinline__ void finish_void() { action = kFinish; }
     __device__ __forceinline__ void bad_state() { action = kFinish; err = GTAP_E_BAD_STATE; }
 };
 
 constexpr uint32_t kHeavyBit = 0x80000000u;  // transient flag on runnable IDs (IDs < 2^31)
+constexpr uint32_t kPendMask = 0x00FFFFFFu;  // join word: count in bits 0-23, resume queue in 24-31
 
 // Placement hint (semantics-free, like EPAQ's queue choice P:990): a table may
 // mark tasks "heavy" (e.g. a mergesort subtree whose merges are large) so the
@@ -72,14 +94,34 @@ __device__ __forceinline__ bool parent_is_heavy(uint32_t child_fn, const uint32_
     if constexpr (T::kHasHeavy) return T::heavy_parent(child_fn, child_d);
     else return false;
 }
+template <class T, class = void>
+struct num_queues_of { static constexpr int value = 1; };
+template <class T>
+struct num_queues_of<T, decltype((void)T::kNumQueues, void())> { static constexpr int value = T::kNumQueues; };
+
+// per-queue owner state lives in registers; q is warp-uniform, the loops unroll to selects
+template <int NQ>
+__device__ __forceinline__ uint32_t qget(const uint32_t (&a)[NQ], uint32_t q) {
+    uint32_t v = a[0];
+#pragma unroll
+    for (int i = 1; i < NQ; ++i) if (q == (uint32_t)i) v = a[i];
+    return v;
+}
+template <int NQ>
+__device__ __forceinline__ void qset(uint32_t (&a)[NQ], uint32_t q, uint32_t v) {
+#pragma unroll
+    for (int i = 0; i < NQ; ++i) if (q == (uint32_t)i) a[i] = v;
+}
 
 template <int MAXC>
 struct WarpSmem {
     uint32_t kept[32];          // keep-for-next-cycle set
     uint32_t fbuf[32];          // records freed this cycle (reused first)
     uint32_t abuf[32 * MAXC];   // records drawn from the free ring / bump region
-    uint32_t cbuf[32 * MAXC];   // child IDs spawned this cycle, spawn order
-    uint32_t pbuf[32];          // parents made runnable this cycle
+    uint32_t cbuf[32 * MAXC];   // child IDs spawned this cycle, spawn order (generic path)
+    uint32_t pbuf[32];          // parents made runnable this cycle (generic path)
+    uint8_t cqb[32 * MAXC];     // queue of each cbuf entry (EPAQ)
+    uint8_t pqb[32];            // queue of each pbuf entry (EPAQ)
 };
 
 template <class T>
@@ -91,6 +133,8 @@ template <class T>
 __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_kernel(KParams p, typename T::Args args) {
     using namespace dev;
     constexpr int MAXC = T::kMaxChildren;
+    constexpr int NQ = num_queues_of<T>::value;
+    constexpr bool kGeneric = T::kHasHeavy || NQ > 1;  // placement through smem lists
     using Out = TOut<MAXC>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
 
@@ -106,14 +150,17 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
 
     const uint32_t M = 1u << p.logM, mmask = M - 1u;
     const uint32_t Q = p.qmask + 1u, qmask = p.qmask;
-    uint32_t* ring = p.ring + (size_t)w * Q;
-    DequeMeta* mydq = p.dq + w;
+    // deque (w, q) is number w * p.nq + q (p.nq >= NQ: the workspace may hold more queues)
+    const uint32_t dq0 = w * p.nq;
     uint32_t* myfring = p.fring + ((size_t)w << p.logM);
     const uint32_t base_id = w << p.logM;
     const uint32_t lt = lanemask_lt();
 
     // owner-local deque / pool state (warp-uniform, in registers)
-    uint32_t tail = 0, split = 0, sdone = 0;
+    uint32_t tail[NQ], split[NQ], sdone[NQ];
+#pragma unroll
+    for (int i = 0; i < NQ; ++i) tail[i] = split[i] = sdone[i] = 0;
+    uint32_t qc = 0;  // queue of the tasks in hand (EPAQ round-robin position)
     uint32_t bump = 0, fhead = 0;
     uint32_t nkept = 0;
     uint32_t rng = hash32(p.seed * 0x9E3779B97F4A7C15ull + (unsigned long long)w * 32u + lane);
@@ -124,13 +171,14 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
     uint32_t cyc_u = 0;  // warp-uniform cycle counter (every lane increments it)
     bool failed = false;
 
-    // ---- entry: roots r = w, w + W, ... go to this warp's deque
+    // ---- entry: roots r = w, w + W, ... go to this warp's queue 0
     {
         uint32_t mine = p.nroots > w ? (p.nroots - w + p.W - 1) / p.W : 0;
         if (mine > M || mine > Q) {
             if (lane == 0) raise_error(p.ctl, GTAP_E_POOL_EXHAUSTED);
             mine = 0;
         }
+        uint32_t* ring0 = p.ring + (size_t)dq0 * Q;
         for (uint32_t i = lane; i < mine; i += 32) {
             const uint32_t r = w + i * p.W;
             const RootSpec rs = p.roots[r];
@@ -138,10 +186,10 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
             TaskRec* rec = p.rec + id;
             st_v4(rec, make_uint4(0u, 0u, make_meta(rs.fn, 0, 0, 0), kRootFlag | r));
             st_v4(&rec->d[0], make_uint4(rs.d[0], rs.d[1], rs.d[2], rs.d[3]));
-            ring[i & qmask] = id;
+            ring0[i & qmask] = id;
         }
         bump = mine;
-        tail = mine;
+        tail[0] = mine;
         st_tasks += (lane == 0) ? mine : 0;
         __syncwarp();
     }
@@ -150,73 +198,93 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
         // ================= (1) acquire =================
         uint32_t n = nkept;
         uint32_t my = (lane < n) ? (sm.kept[lane] & ~kHeavyBit) : kNone;
-        unsigned long long S_seen = 0;
+        // lane q holds the own S word of queue q (used for reclaim and the publication check)
+        unsigned long long S_lane = 0;
         uint32_t done_seen = 0;
-        if (lane == 0) {
-            S_seen = ld_relaxed(&mydq->S);
-            done_seen = ld_relaxed(&p.ctl->done);
-        }
+        if (lane < (uint32_t)NQ) S_lane = ld_relaxed(&p.dq[dq0 + lane].S);
+        if (lane == 31) done_seen = ld_relaxed(&p.ctl->done);
         if (lane == 0) st_kept += n;
-        // LIFO pop from the private part: no atomics (owner only)
-        {
-            const uint32_t priv = tail - split;
-            if (n < 32 && priv > 0) {
-                const uint32_t c = min(32u - n, priv);
-                if (lane >= n && lane < n + c) my = ld_relaxed(&ring[(tail - 1u - (lane - n)) & qmask]);
-                tail -= c;
-                n += c;
-                if (lane == 0) st_pops += c;
-            }
-        }
-        // reclaim from the own public part (only when nothing else to run)
-        if (n == 0) {
-            uint32_t got = 0, s_new = 0;
-            if (lane == 0) {
-                unsigned long long s = S_seen;
-                for (int it = 0; it < 8; ++it) {
-                    const uint32_t h = (uint32_t)s, sp = (uint32_t)(s >> 32);
-                    const uint32_t avail = sp - h;
-                    if (avail == 0u || avail > Q) break;
-                    // a small public part (top-of-tree / heavy tasks) is shared: take half (>= 1)
-                    const uint32_t c = avail <= 4u ? max(1u, avail >> 1) : min(32u, avail);
-                    const unsigned long long nw = ((unsigned long long)(sp - c) << 32) | h;
-                    const unsigned long long o = atom_cas_relaxed(&mydq->S, s, nw);
-                    if (o == s) { got = c; s_new = sp - c; break; }
-                    s = o;
+        // LIFO pop from a private part, round-robin over the queues from qc: no atomics (owner only)
+        if (n < 32) {
+#pragma unroll
+            for (int k = 0; k < NQ; ++k) {
+                const uint32_t q = (qc + (uint32_t)k) % (uint32_t)NQ;
+                // kept tasks are of queue qc: only top them up from qc itself
+                if (k > 0 && n > 0) break;
+                const uint32_t tq = qget(tail, q);
+                const uint32_t priv = tq - qget(split, q);
+                if (priv > 0) {
+                    const uint32_t c = min(32u - n, priv);
+                    uint32_t* ringq = p.ring + (size_t)(dq0 + q) * Q;
+                    if (lane >= n && lane < n + c) my = ld_relaxed(&ringq[(tq - 1u - (lane - n)) & qmask]);
+                    qset(tail, q, tq - c);
+                    n += c;
+                    qc = q;
+                    if (lane == 0) st_pops += c;
+                    break;
                 }
             }
-            got = __shfl_sync(0xffffffffu, got, 0);
-            s_new = __shfl_sync(0xffffffffu, s_new, 0);
-            if (got) {
-                split = s_new;
-                tail = s_new;
-                if (lane < got) my = ld_relaxed(&ring[(s_new + got - 1u - lane) & qmask]);
-                n = got;
-                if (lane == 0) st_pops += got;
+        }
+        // reclaim from an own public part (only when nothing else to run)
+        if (n == 0) {
+#pragma unroll
+            for (int k = 0; k < NQ; ++k) {
+                const uint32_t q = (qc + (uint32_t)k) % (uint32_t)NQ;
+                const unsigned long long sq = __shfl_sync(0xffffffffu, S_lane, q);
+                uint32_t got = 0, s_new = 0;
+                if (lane == 0) {
+                    unsigned long long s = sq;
+                    for (int it = 0; it < 8; ++it) {
+                        const uint32_t h = (uint32_t)s, sp = (uint32_t)(s >> 32);
+                        const uint32_t avail = sp - h;
+                        if (avail == 0u || avail > Q) break;
+                        // a small public part (top-of-tree / heavy tasks) is shared: take half (>= 1)
+                        const uint32_t c = avail <= 4u ? max(1u, avail >> 1) : min(32u, avail);
+                        const unsigned long long nw = ((unsigned long long)(sp - c) << 32) | h;
+                        const unsigned long long o = atom_cas_relaxed(&p.dq[dq0 + q].S, s, nw);
+                        if (o == s) { got = c; s_new = sp - c; break; }
+                        s = o;
+                    }
+                }
+                got = __shfl_sync(0xffffffffu, got, 0);
+                s_new = __shfl_sync(0xffffffffu, s_new, 0);
+                if (got) {
+                    qset(split, q, s_new);
+                    qset(tail, q, s_new);
+                    uint32_t* ringq = p.ring + (size_t)(dq0 + q) * Q;
+                    if (lane < got) my = ld_relaxed(&ringq[(s_new + got - 1u - lane) & qmask]);
+                    n = got;
+                    qc = q;
+                    if (lane == 0) st_pops += got;
+                    break;
+                }
             }
         }
-        // steal: probe 32 random victims in parallel, claim from the fullest
+        // steal: probe 32 random (victim, queue) pairs in parallel, claim from the fullest
         if (n == 0 && p.W > 1) {
             // a long-idle warp probes once per wake-up (keeps idle L2 traffic off busy workers)
             const uint32_t rounds = backoff >= 4096u ? 1u : p.steal_rounds;
             for (uint32_t round = 0; round < rounds && n == 0; ++round) {
                 uint32_t v = xorshift32(rng) % (p.W - 1u);
                 v += (v >= w);
-                const unsigned long long sv = ld_relaxed(&p.dq[v].S);
+                const uint32_t vq = (qc + lane) % (uint32_t)NQ;  // EPAQ: round-robin from the own position
+                const uint32_t vd = v * p.nq + vq;
+                const unsigned long long sv = ld_relaxed(&p.dq[vd].S);
                 uint32_t avail = (uint32_t)(sv >> 32) - (uint32_t)sv;
                 if (avail > Q) avail = 0;
                 // warp arg-max over (avail, lane)
-                uint32_t best = (avail << 5) | lane;
+                uint32_t best = (min(avail, (1u << 26)) << 5) | lane;
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
                 if ((best >> 5) == 0) { if (lane == 0) ++st_sfail; continue; }
                 const uint32_t bl = best & 31u;
-                const uint32_t victim = __shfl_sync(0xffffffffu, v, bl);
-                DequeMeta* vdq = p.dq + victim;
+                const uint32_t vdq = __shfl_sync(0xffffffffu, vd, bl);
+                const uint32_t vqq = __shfl_sync(0xffffffffu, vq, bl);
+                DequeMeta* vm = p.dq + vdq;
                 uint32_t got = 0, h0 = 0;
                 if (lane == 0) {
-                    if (atom_cas_relaxed(&vdq->lock, 0u, 1u) == 0u) {  // try-lock
-                        unsigned long long s = ld_relaxed(&vdq->S);
+                    if (atom_cas_relaxed(&vm->lock, 0u, 1u) == 0u) {  // try-lock
+                        unsigned long long s = ld_relaxed(&vm->S);
                         for (int it = 0; it < 8; ++it) {
                             const uint32_t h = (uint32_t)s, sp = (uint32_t)(s >> 32);
                             const uint32_t a = sp - h;
@@ -224,32 +292,33 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
                             // claim up to steal_max; half of a small public part
                             const uint32_t c = a <= 4u ? (a + 1u) >> 1 : min(p.steal_max, a);
                             const unsigned long long nw = ((unsigned long long)sp << 32) | (uint32_t)(h + c);
-                            const unsigned long long o = atom_cas_acquire(&vdq->S, s, nw);
+                            const unsigned long long o = atom_cas_acquire(&vm->S, s, nw);
                             if (o == s) { got = c; h0 = h; break; }
                             s = o;
                         }
-                        if (got == 0u) st_relaxed(&vdq->lock, 0u);
+                        if (got == 0u) st_relaxed(&vm->lock, 0u);
                     }
                 }
                 got = __shfl_sync(0xffffffffu, got, 0);
                 h0 = __shfl_sync(0xffffffffu, h0, 0);
                 if (got) {
                     // advance the read prefix only after loading the stolen IDs
-                    if (lane < got) my = ld_relaxed(&p.ring[(size_t)victim * Q + ((h0 + lane) & qmask)]);
+                    if (lane < got) my = ld_relaxed(&p.ring[(size_t)vdq * Q + ((h0 + lane) & qmask)]);
                     __syncwarp();
                     if (lane == 0) {
-                        red_add_release(&vdq->steal_done, got);
-                        st_relaxed(&vdq->lock, 0u);
+                        red_add_release(&vm->steal_done, got);
+                        st_relaxed(&vm->lock, 0u);
                         ++st_sok;
                         st_stolen += got;
                     }
                     n = got;
+                    qc = vqq;
                 } else if (lane == 0) {
                     ++st_sfail;
                 }
             }
         }
-        done_seen = __shfl_sync(0xffffffffu, done_seen, 0);
+        done_seen = __shfl_sync(0xffffffffu, done_seen, 31);
         if (n == 0) {
             // idle: termination check + watchdog + backoff
             if (lane == 0) ++st_idle;
@@ -280,6 +349,12 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
             myfn = meta_fn(h.z);
             T::exec(args, meta_fn(h.z), meta_state(h.z), d, o, bx);
             if (o.action == 0u) o.err = GTAP_E_BAD_STATE;
+            if (NQ > 1) {  // queue(expr) out of range is a usage error
+                if (o.action == Out::kSuspend && o.next_queue >= (uint32_t)NQ) o.err = GTAP_E_INVAL;
+#pragma unroll
+                for (int c = 0; c < MAXC; ++c)
+                    if ((uint32_t)c < o.nchild && o.cq[c] >= (uint32_t)NQ) o.err = GTAP_E_INVAL;
+            }
         }
         __syncwarp();
         uint32_t err = o.err;
@@ -338,17 +413,23 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
                 const uint32_t g = excl + c;
                 cid[c] = (g < fromF) ? sm.fbuf[g] : sm.abuf[g - fromF];
                 TaskRec* cr = p.rec + cid[c];
-                st_v4(cr, make_uint4(0u, 0u, make_meta(o.cfn[c], 0, c, 0), T::kTaskwait ? my : kNone));
+                st_v4(cr, make_uint4(0u, 0u, make_meta(o.cfn[c], 0, c, o.cq[c]), T::kTaskwait ? my : kNone));
                 st_v4(&cr->d[0], make_uint4(o.cd[c][0], o.cd[c][1], o.cd[c][2], o.cd[c][3]));
-                if constexpr (T::kHasHeavy)
+                if constexpr (kGeneric) {
                     sm.cbuf[g] = cid[c] | (task_is_heavy<T>(o.cfn[c], o.cd[c]) ? kHeavyBit : 0u);
+                    sm.cqb[g] = (uint8_t)o.cq[c];
+                }
             }
         }
-        // suspend: store the resumption state and the join counter
-        uint32_t resume_id = kNone;
+        // suspend: store the resumption state and the join counter; the taskwait
+        // queue(expr) rides in the top byte of the join word (EPAQ)
+        uint32_t resume_id = kNone, resume_q = 0;
         if (o.action == Out::kSuspend) {
-            st_v4(p.rec + my, make_uint4(nc, 0u, make_meta(myfn, o.next_state, ord, 0), parent));
-            if (nc == 0u) resume_id = my | (task_is_heavy<T>(myfn, mydata) ? kHeavyBit : 0u);  // empty join
+            st_v4(p.rec + my, make_uint4(nc | (o.next_queue << 24), 0u, make_meta(myfn, o.next_state, ord, 0), parent));
+            if (nc == 0u) {  // empty join: runnable at once
+                resume_id = my | (task_is_heavy<T>(myfn, mydata) ? kHeavyBit : 0u);
+                resume_q = o.next_queue;
+            }
         }
         // surplus freed records go back to their home worker's free ring
         if (F > T_total) {
@@ -378,21 +459,27 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
         if (fin && err == 0u) {
             if (parent != kNone && !is_root_link(parent)) {
                 bool last;
+                uint32_t pend_old;
                 if constexpr (T::kJoinReduceAdd) {
-                    // one relaxed 64-bit RMW: pending -= 1 and acc += result (the low word never
+                    // one relaxed 64-bit RMW: pending -= 1 and acc += result (the count never
                     // underflows, so adding 0xFFFFFFFF carries exactly once into acc: add result - 1)
                     const unsigned long long inc =
                         ((unsigned long long)(uint32_t)(o.result - 1) << 32) | 0xFFFFFFFFull;
                     const unsigned long long old = atom_add_relaxed_u64(&p.rec[parent], inc);
-                    last = (uint32_t)old == 1u;
+                    pend_old = (uint32_t)old;
+                    last = (pend_old & kPendMask) == 1u;
                     if (last) {  // the continuation reads the sum as load_result(0) + load_result(1)
                         const uint32_t sum = (uint32_t)(old >> 32) + (uint32_t)o.result;
                         st_v2(&p.rec[parent].d[2], sum, 0u);
                     }
                 } else {
-                    last = atom_add_acq_rel(&p.rec[parent].pending, -1) == 1;
+                    pend_old = (uint32_t)atom_add_acq_rel(&p.rec[parent].pending, -1);
+                    last = (pend_old & kPendMask) == 1u;
                 }
-                if (last) resume_id = parent | (parent_is_heavy<T>(myfn, mydata) ? kHeavyBit : 0u);
+                if (last) {
+                    resume_id = parent | (parent_is_heavy<T>(myfn, mydata) ? kHeavyBit : 0u);
+                    resume_q = pend_old >> 24;
+                }
             } else if (is_root_link(parent)) {
                 const uint32_t r = parent & ~kRootFlag;
                 p.root_results[r] = o.has_result ? (long long)o.result : 0ll;
@@ -418,91 +505,137 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
         const uint32_t rball = __ballot_sync(0xffffffffu, resume_id != kNone);
         const uint32_t P = __popc(rball);
         const uint32_t R = P + T_total;
-        uint32_t keep = 0, pushc = 0, heavy_pushed = 0;
-        if constexpr (!T::kHasHeavy) {
+        uint32_t keep = 0, pushc = 0;
+        uint32_t pushq[NQ];      // pushed per queue (uniform)
+        uint32_t heavy_q = 0;    // bit q: a heavy task was pushed to queue q
+#pragma unroll
+        for (int i = 0; i < NQ; ++i) pushq[i] = 0;
+        if constexpr (!kGeneric) {
             // runnable list = [resumed parents in lane order, children in spawn order]; the first 32
             // are kept, entry e >= 32 goes to ring slot tail + e - 32: every lane places its own
             keep = min(R, 32u);
             pushc = R - keep;
-            if (pushc && tail + pushc - sdone > Q) {
-                if (lane == 0) sdone = ld_relaxed(&mydq->steal_done);
-                sdone = __shfl_sync(0xffffffffu, sdone, 0);
-                if (tail + pushc - sdone > Q) {
+            pushq[0] = pushc;
+            if (pushc && tail[0] + pushc - sdone[0] > Q) {
+                if (lane == 0) sdone[0] = ld_relaxed(&p.dq[dq0].steal_done);
+                sdone[0] = __shfl_sync(0xffffffffu, sdone[0], 0);
+                if (tail[0] + pushc - sdone[0] > Q) {
                     if (lane == 0) raise_error(p.ctl, GTAP_E_QUEUE_OVERFLOW);
                     break;
                 }
             }
+            uint32_t* ring0 = p.ring + (size_t)dq0 * Q;
             if (resume_id != kNone) sm.kept[__popc(rball & lt)] = resume_id;
 #pragma unroll
             for (int c = 0; c < MAXC; ++c) {
                 if ((uint32_t)c < nc) {
                     const uint32_t e = P + excl + c;
                     if (e < 32u) sm.kept[e] = cid[c];
-                    else ring[(tail + (e - 32u)) & qmask] = cid[c];
+                    else ring0[(tail[0] + (e - 32u)) & qmask] = cid[c];
                 }
             }
         } else {
-            // keep <= 32 runnable tasks (resumed parents first, then children); tasks the table
-            // marks heavy are never kept: they are pushed and published so idle warps take them
-            if (resume_id != kNone) sm.pbuf[__popc(rball & lt)] = resume_id;
+            // generic placement (heavy hints and/or EPAQ): the kept set holds up to 32 light tasks of
+            // ONE queue class in list order (resumed parents first, then children); every
+            // other task goes to the tail of its own queue
+            if (resume_id != kNone) {
+                sm.pbuf[__popc(rball & lt)] = resume_id;
+                sm.pqb[__popc(rball & lt)] = (uint8_t)resume_q;
+            }
             __syncwarp();
+            // EPAQ: the class of the next cycle is the next queue in round-robin order;
+            // the kept set holds this cycle's new tasks of that class, so every class -- including
+            // continuations, which free records -- is visited every NQ cycles
+            const uint32_t qk = NQ > 1 ? (qc + 1u) % (uint32_t)NQ : 0u;
+            // pass 1: count pushes per queue (capacity check before any ring write)
             for (uint32_t base = 0; base < R; base += 32) {
                 const uint32_t i = base + lane;
-                uint32_t id = kNone;
-                if (i < R) id = (i < P) ? sm.pbuf[i] : sm.cbuf[i - P];
+                uint32_t id = kNone, qi = 0;
+                if (i < R) {
+                    id = (i < P) ? sm.pbuf[i] : sm.cbuf[i - P];
+                    qi = NQ > 1 ? ((i < P) ? sm.pqb[i] : sm.cqb[i - P]) : 0u;
+                }
                 const bool hv = (i < R) && (id & kHeavyBit);
-                const uint32_t light = __ballot_sync(0xffffffffu, i < R && !hv);
-                const uint32_t lrank = keep + __popc(light & lt);
-                const bool k = (i < R) && !hv && lrank < 32u;
-                const uint32_t kb = __ballot_sync(0xffffffffu, k);
-                const uint32_t pb = __ballot_sync(0xffffffffu, i < R && !k);
-                if (k) sm.kept[lrank] = id;
-                if (i < R && !k) {
-                    const uint32_t slot = tail + pushc + __popc(pb & lt);
-                    if (slot - sdone < Q) ring[slot & qmask] = id & ~kHeavyBit;
-                }
-                keep += __popc(kb);
-                pushc += __popc(pb);
-                heavy_pushed |= __ballot_sync(0xffffffffu, hv);
-            }
-            if (pushc && tail + pushc - sdone > Q) {
-                if (lane == 0) sdone = ld_relaxed(&mydq->steal_done);
-                sdone = __shfl_sync(0xffffffffu, sdone, 0);
-                if (tail + pushc - sdone > Q) {
-                    if (lane == 0) raise_error(p.ctl, GTAP_E_QUEUE_OVERFLOW);
-                    break;
-                }
-                // capacity was only stale: write the entries skipped above
-                for (uint32_t base = 0, kk = 0, pc = 0; base < R; base += 32) {
-                    const uint32_t i = base + lane;
-                    uint32_t id = kNone;
-                    if (i < R) id = (i < P) ? sm.pbuf[i] : sm.cbuf[i - P];
-                    const bool hv = (i < R) && (id & kHeavyBit);
-                    const uint32_t light = __ballot_sync(0xffffffffu, i < R && !hv);
-                    const bool k = (i < R) && !hv && (kk + __popc(light & lt)) < 32u;
-                    const uint32_t pb = __ballot_sync(0xffffffffu, i < R && !k);
-                    if (i < R && !k) ring[(tail + pc + __popc(pb & lt)) & qmask] = id & ~kHeavyBit;
-                    kk += __popc(__ballot_sync(0xffffffffu, k));
-                    pc += __popc(pb);
+                const bool cand = (i < R) && !hv && qi == qk;
+                const uint32_t cb = __ballot_sync(0xffffffffu, cand);
+                const bool k = cand && (keep + __popc(cb & lt)) < 32u;
+                keep += min(__popc(cb), 32u - min(keep, 32u));
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) {
+                    const uint32_t pb = __ballot_sync(0xffffffffu, i < R && !k && qi == (uint32_t)q);
+                    pushq[q] += __popc(pb);
+                    if (__ballot_sync(0xffffffffu, i < R && !k && hv && qi == (uint32_t)q)) heavy_q |= 1u << q;
                 }
             }
+            bool overflow = false;
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                if (pushq[q] && tail[q] + pushq[q] - sdone[q] > Q) {
+                    if (lane == 0) sdone[q] = ld_relaxed(&p.dq[dq0 + q].steal_done);
+                    sdone[q] = __shfl_sync(0xffffffffu, sdone[q], 0);
+                    if (tail[q] + pushq[q] - sdone[q] > Q) overflow = true;
+                }
+            }
+            if (overflow) {
+                if (lane == 0) raise_error(p.ctl, GTAP_E_QUEUE_OVERFLOW);
+                break;
+            }
+            // pass 2: place
+            uint32_t kk = 0;
+            uint32_t pc[NQ];
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) pc[q] = 0;
+            for (uint32_t base = 0; base < R; base += 32) {
+                const uint32_t i = base + lane;
+                uint32_t id = kNone, qi = 0;
+                if (i < R) {
+                    id = (i < P) ? sm.pbuf[i] : sm.cbuf[i - P];
+                    qi = NQ > 1 ? ((i < P) ? sm.pqb[i] : sm.cqb[i - P]) : 0u;
+                }
+                const bool hv = (i < R) && (id & kHeavyBit);
+                const bool cand = (i < R) && !hv && qi == qk;
+                const uint32_t cb = __ballot_sync(0xffffffffu, cand);
+                const uint32_t rank = kk + __popc(cb & lt);
+                const bool k = cand && rank < 32u;
+                if (k) sm.kept[rank] = id;
+                kk += min(__popc(cb), 32u - min(kk, 32u));
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) {
+                    const uint32_t pb = __ballot_sync(0xffffffffu, i < R && !k && qi == (uint32_t)q);
+                    if (i < R && !k && qi == (uint32_t)q) {
+                        uint32_t* ringq = p.ring + (size_t)(dq0 + q) * Q;
+                        ringq[(tail[q] + pc[q] + __popc(pb & lt)) & qmask] = id & ~kHeavyBit;
+                    }
+                    pc[q] += __popc(pb);
+                }
+            }
+            pushc = 0;
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) pushc += pushq[q];
+            qc = qk;  // next cycle runs the kept class (or pops from it first)
         }
         __syncwarp();
-        tail += pushc;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) tail[q] += pushq[q];
         nkept = keep;
         if (lane == 0) st_push += pushc;
-        // publish the oldest half of the private part when thieves drained the public part,
-        // or everything at once when heavy tasks were just pushed
-        if (lane == 0) {
-            const uint32_t h = (uint32_t)S_seen;
-            const uint32_t priv = tail - split;
-            if ((heavy_pushed && priv) || (h == split && priv >= 2u)) {
-                const uint32_t k = heavy_pushed ? priv : (priv >> 1);
-                split += k;
-                red_add_release(&mydq->S, (unsigned long long)k << 32);
+        // publish the oldest half of a private part when thieves drained its public part,
+        // or all of it when heavy tasks were just pushed there
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            const unsigned long long sq = __shfl_sync(0xffffffffu, S_lane, q);
+            if (lane == 0) {
+                const uint32_t h = (uint32_t)sq;
+                const uint32_t priv = tail[q] - split[q];
+                const bool hvq = (heavy_q >> q) & 1u;
+                if ((hvq && priv) || (h == split[q] && priv >= 2u)) {
+                    const uint32_t k = hvq ? priv : (priv >> 1);
+                    split[q] += k;
+                    red_add_release(&p.dq[dq0 + q].S, (unsigned long long)k << 32);
+                }
             }
+            split[q] = __shfl_sync(0xffffffffu, split[q], 0);
         }
-        split = __shfl_sync(0xffffffffu, split, 0);
         __syncwarp();
         if (done_seen) break;  // error raised elsewhere (completion implies no tasks left)
         if (p.watchdog_ns && ((++cyc_u) & 4095u) == 0u) {

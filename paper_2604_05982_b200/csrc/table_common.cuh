@@ -16,6 +16,7 @@ struct gtap_task_table {
     uint32_t max_children;  // compile-time bound of the table (GTAP_MAX_CHILD_TASKS)
     uint32_t nfn;           // number of task functions
     uint32_t max_block;     // __launch_bounds__ max threads of the table's kernel
+    uint32_t num_queues;    // EPAQ queues the table routes tasks to (1 = no EPAQ)
     const char* name;
     cudaError_t (*launch)(const gtap_task_table*, const gtap::KParams&, uint32_t grid, uint32_t block,
                           cudaStream_t);
@@ -81,6 +82,8 @@ gtap_task_table* make_table(const char* name, const typename T::Args& a,
     t->max_children = (uint32_t)T::kMaxChildren;
     t->nfn = T::kNumFn;
     t->max_block = (uint32_t)T::kMaxThreads;
+    if constexpr (T::kKind == GTAP_WORKER_THREAD) t->num_queues = (uint32_t)num_queues_of<T>::value;
+    else t->num_queues = 1;
     t->name = name;
     if constexpr (T::kKind == GTAP_WORKER_THREAD) {
         t->launch = &launch_thread<T>;

@@ -62,7 +62,8 @@ class Stats(ctypes.Structure):
 EXPORTS = [
     "gtap_abi_version", "gtap_status_str", "gtap_config_default", "gtap_workspace_bytes", "gtap_init",
     "gtap_spawn_root", "gtap_reset", "gtap_run", "gtap_sync", "gtap_root_result", "gtap_finalize",
-    "gtap_geometry", "gtap_table_destroy", "gtap_table_fib", "gtap_table_mergesort", "gtap_table_spmv",
+    "gtap_geometry", "gtap_table_destroy", "gtap_table_fib", "gtap_table_fib_cutoff", "gtap_table_mergesort",
+    "gtap_table_spmv",
     "gtap_table_bfs", "gtap_bfs_init_depth", "gtap_ubench_atomics",
 ]
 
@@ -97,6 +98,8 @@ def lib():
     L.gtap_table_destroy.restype = None
     L.gtap_table_fib.argtypes = []
     L.gtap_table_fib.restype = vp
+    L.gtap_table_fib_cutoff.argtypes = [i32, u32]
+    L.gtap_table_fib_cutoff.restype = vp
     L.gtap_table_mergesort.argtypes = [vp, vp, u64, i32]
     L.gtap_table_mergesort.restype = vp
     L.gtap_table_spmv.argtypes = [vp, vp, vp, vp, vp, u32, u32, u32]
@@ -155,6 +158,11 @@ class Table:
         return Table(lib().gtap_table_fib(), "fib", GTAP_WORKER_THREAD)
 
     @staticmethod
+    def fib_cutoff(cutoff: int, num_queues: int = 1) -> "Table":
+        """fib with a cutoff; num_queues=3 routes tasks with the paper's EPAQ classifier."""
+        return Table(lib().gtap_table_fib_cutoff(cutoff, num_queues), "fib_cutoff", GTAP_WORKER_THREAD)
+
+    @staticmethod
     def mergesort(keys, scratch, cutoff: int = 128) -> "Table":
         _dev_i32(keys, "keys"); _dev_i32(scratch, "scratch")
         if scratch.numel() < keys.numel():
@@ -211,7 +219,7 @@ class Runtime:
     def __init__(self, kind: int, device: int = 0, *, grid_size: int = 0, block_size: int = 0,
                  max_tasks_per_worker: int = 0, queue_capacity: int = 0, steal_attempts: int = 0,
                  steal_max: int = 0, seed: int = 0x5EED, watchdog_ns: int = 0, max_roots: int = 0,
-                 idle_backoff_ns: int = 0,
+                 idle_backoff_ns: int = 0, num_queues: int = 0,
                  torch_workspace: bool = True):
         import torch
         L = lib()
@@ -219,7 +227,8 @@ class Runtime:
         _check(L.gtap_config_default(ctypes.byref(cfg), device, kind), "gtap_config_default")
         for k, v in dict(grid_size=grid_size, block_size=block_size, max_tasks_per_worker=max_tasks_per_worker,
                          queue_capacity=queue_capacity, steal_attempts=steal_attempts, steal_max=steal_max,
-                         watchdog_ns=watchdog_ns, max_roots=max_roots, idle_backoff_ns=idle_backoff_ns).items():
+                         watchdog_ns=watchdog_ns, max_roots=max_roots, idle_backoff_ns=idle_backoff_ns,
+                         num_queues=num_queues).items():
             if v:
                 setattr(cfg, k, v)
         cfg.seed = seed

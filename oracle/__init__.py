@@ -39,6 +39,8 @@ def lib():
         L.oracle_fib.argtypes = [ctypes.c_int32, i64p, i64p, i64p]
         L.oracle_fib_cutoff.argtypes = [ctypes.c_int32, ctypes.c_int32, i64p, i64p, i64p, i64p]
         L.oracle_fib_cutoff.restype = ctypes.c_int
+        L.oracle_nqueens.argtypes = [ctypes.c_int32, ctypes.c_int32, i64p, i64p]
+        L.oracle_nqueens.restype = ctypes.c_int
         L.oracle_mergesort.argtypes = [vp, vp, ctypes.c_int64, ctypes.c_int64, i64p, i64p]
         L.oracle_spmv.argtypes = [vp, vp, vp, vp, ctypes.c_int64, vp, vp]
         L.oracle_bfs.argtypes = [vp, vp, ctypes.c_int64, ctypes.c_int32, vp]
@@ -75,6 +77,14 @@ def fib_cutoff(n: int, cutoff: int):
     if rc != 0:
         raise ValueError(f"fib_cutoff: bad arguments n={n} cutoff={cutoff}")
     return v.value, t.value, i.value, c.value
+
+
+def nqueens(n: int, cutoff: int = 7):
+    """(solutions, tasks) of the bitmask N-Queens task program with a cutoff depth."""
+    v, t = ctypes.c_int64(), ctypes.c_int64()
+    if lib().oracle_nqueens(n, cutoff, ctypes.byref(v), ctypes.byref(t)) != 0:
+        raise ValueError("nqueens: bad arguments")
+    return v.value, t.value
 
 
 def mergesort(keys, cutoff: int = 128):

@@ -91,6 +91,53 @@ int oracle_fib_cutoff(int32_t n, int32_t cutoff, int64_t *value, int64_t *tasks,
     return 0;
 }
 
+/* ------------------------------------------------------------- N-Queens */
+/*
+ * N-Queens by bitmask backtracking with a cutoff depth (PAPER.md P:465,
+ * "count solutions via bitmask-based backtracking with a fixed
+ * cutoff depth (7)", no taskwait): a task at row r < cutoff spawns one child
+ * task per free column of row r; a task at row >= cutoff counts the solutions
+ * below it serially; the counts are summed (no join needed). Reading R25:
+ * cols / left / right diagonals as bitmasks, the diagonals shifted per row.
+ */
+static int64_t nq_serial(int32_t n, int32_t row, uint32_t cols, uint32_t d1, uint32_t d2)
+{
+    if (row == n) return 1;
+    const uint32_t full = (n >= 32) ? 0xFFFFFFFFu : ((1u << n) - 1u);
+    uint32_t avail = ~(cols | d1 | d2) & full;
+    int64_t c = 0;
+    while (avail) {
+        uint32_t bit = avail & (0u - avail);
+        avail ^= bit;
+        c += nq_serial(n, row + 1, cols | bit, (d1 | bit) << 1, (d2 | bit) >> 1);
+    }
+    return c;
+}
+
+static int64_t nq_task(int32_t n, int32_t cutoff, int32_t row, uint32_t cols, uint32_t d1, uint32_t d2,
+                       int64_t *tasks)
+{
+    *tasks += 1;
+    if (row == n || row >= cutoff) return nq_serial(n, row, cols, d1, d2);
+    const uint32_t full = (n >= 32) ? 0xFFFFFFFFu : ((1u << n) - 1u);
+    uint32_t avail = ~(cols | d1 | d2) & full;
+    int64_t c = 0;
+    while (avail) {
+        uint32_t bit = avail & (0u - avail);
+        avail ^= bit;
+        c += nq_task(n, cutoff, row + 1, cols | bit, (d1 | bit) << 1, (d2 | bit) >> 1, tasks);
+    }
+    return c;
+}
+
+int oracle_nqueens(int32_t n, int32_t cutoff, int64_t *solutions, int64_t *tasks)
+{
+    if (n < 1 || n > 32 || cutoff < 0) return -1;
+    *tasks = 0;
+    *solutions = nq_task(n, cutoff, 0, 0u, 0u, 0u, tasks);
+    return 0;
+}
+
 /* ------------------------------------------------------------ mergesort */
 /*
  * P:153-165 (Prog. cutoff mergesort, §4.4) with the state machine of

@@ -43,6 +43,9 @@ SPMV_ROWS = 1 << 22
 SPMV_NNZ_CUT = 8192
 SPMV_FANOUT = 32
 SPMV_CFG = dict(grid_size=148 * 8, block_size=128, max_tasks_per_worker=1024)
+NQ_N = 16
+NQ_CUTOFF = 7
+NQ_CFG = dict(grid_size=0, block_size=128, max_tasks_per_worker=4096)
 BFS_SCALE = 22
 BFS_CFG = dict(grid_size=148 * 4, block_size=256, max_tasks_per_worker=1 << 19, idle_backoff_ns=1024)
 
@@ -278,6 +281,21 @@ def bench_epaq(dev, cutoff=10, reps=3):
                 paper="~1.8x on GH200 (P:788)")
 
 
+def bench_nqueens(dev, reps=3):
+    """SURVEY §8(f) NEXT #4: N-Queens n = 16, cutoff depth 7 (P:465, P:588)."""
+    import paper_2604_05982_b200 as g
+    with g.Runtime(g.GTAP_WORKER_THREAD, dev.index, **NQ_CFG) as rt:
+        ms = []
+        for i in range(reps + 1):
+            sol, st = g.nqueens(NQ_N, NQ_CUTOFF, rt=rt)
+            assert sol == 14772512
+            if i:
+                ms.append(st.device_ms)
+    t = statistics.median(ms)
+    return dict(workload="N-Queens n=16 cutoff 7 (NEXT #4), thread-level, no taskwait", metric="tasks/s",
+                value=st.tasks / (t * 1e-3), ms=t, tasks=st.tasks, solutions=sol)
+
+
 def bench_atomics(dev):
     import torch
 
@@ -392,6 +410,7 @@ def run_ours(args):
             secondary.append(fibr)
             secondary.append(dict(workload="L2 atomic probes", metric="ops/s", value=atoms))
             secondary.append(bench_epaq(dev))
+            secondary.append(bench_nqueens(dev))
         except Exception as e:  # secondary results must not kill the main line
             secondary.append(dict(workload="fib40/atomics", error=repr(e)))
         try:

@@ -182,6 +182,12 @@ const gtap_task_table *gtap_table_fib(void);
  * args {int32 n}, 0 <= n <= 46; result int64 fib(n). NULL on bad arguments. */
 const gtap_task_table *gtap_table_fib_cutoff(int32_t cutoff, uint32_t num_queues);
 
+/* N-Queens: bitmask backtracking, one task per free column while
+ * fewer than `cutoff` rows are placed, serial counting below; no taskwait.
+ * n in [1, 20]; d_count: caller-owned device uint64, zeroed by the caller,
+ * receives the number of solutions. fn 0, root args {} (nbytes 0). */
+const gtap_task_table *gtap_table_nqueens(int32_t n, int32_t cutoff, unsigned long long *d_count);
+
 /* mergesort with cutoff (state machine P:59-74), thread-level.
  * keys: int32[n] device buffer sorted in place; scratch: int32[n] device
  * buffer (ping-pong target); cutoff in [1, 256]. fn 0, root args

@@ -17,7 +17,7 @@ from . import gtap
 from .gtap import (GTAP_WORKER_BLOCK, GTAP_WORKER_THREAD, GtapError, Runtime, RunStats, Table,
                    bfs_init_depth, ubench_atomics)
 
-__all__ = ["gtap", "Runtime", "Table", "RunStats", "GtapError", "fib", "fib_cutoff", "mergesort_", "mergesort_forest_",
+__all__ = ["gtap", "Runtime", "Table", "RunStats", "GtapError", "fib", "fib_cutoff", "nqueens", "mergesort_", "mergesort_forest_",
            "spmv", "bfs", "ubench_atomics", "GTAP_WORKER_THREAD", "GTAP_WORKER_BLOCK"]
 
 
@@ -53,6 +53,23 @@ def fib_cutoff(n: int, cutoff: int, num_queues: int = 1, rt: Runtime | None = No
         rt.run(stream)
         st = rt.sync()
         return rt.root_result(0), st
+    finally:
+        table.close()
+        if own:
+            rt.close()
+
+
+def nqueens(n: int, cutoff: int = 7, rt: Runtime | None = None, device: int = 0, stream=None, **cfg):
+    """Number of n-queens solutions by the paper's bitmask task program; returns (count, stats)."""
+    import torch
+    count = torch.zeros(1, dtype=torch.int64, device=f"cuda:{device}")
+    rt, own = _runtime(GTAP_WORKER_THREAD, rt, device, cfg)
+    table = Table.nqueens(n, cutoff, count)
+    try:
+        rt.spawn_root(table, ())
+        rt.run(stream)
+        st = rt.sync()
+        return int(count.item()), st
     finally:
         table.close()
         if own:

@@ -55,6 +55,9 @@ struct TOut {
     uint32_t cfn[MAXC];
     uint32_t cq[MAXC];    // spawn queue(expr) (EPAQ)
     uint32_t cd[MAXC][kDataWords];
+    // generated children (tables with kGenChildren): child c is T::gen_child(gen, gmask, c, ...)
+    uint32_t gen[kDataWords];
+    uint32_t gmask;
     static constexpr uint32_t kFinish = 1, kSuspend = 2;
     __device__ __forceinline__ void init() {
         action = 0; nchild = 0; has_result = 0; err = 0; result = 0; next_state = 0; next_queue = 0;
@@ -94,6 +97,11 @@ __device__ __forceinline__ bool parent_is_heavy(uint32_t child_fn, const uint32_
     if constexpr (T::kHasHeavy) return T::heavy_parent(child_fn, child_d);
     else return false;
 }
+template <class T, class = void>
+struct gen_children_of { static constexpr bool value = false; };
+template <class T>
+struct gen_children_of<T, decltype((void)T::kGenChildren, void())> { static constexpr bool value = T::kGenChildren; };
+
 template <class T, class = void>
 struct num_queues_of { static constexpr int value = 1; };
 template <class T>
@@ -135,7 +143,8 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
     constexpr int MAXC = T::kMaxChildren;
     constexpr int NQ = num_queues_of<T>::value;
     constexpr bool kGeneric = T::kHasHeavy || NQ > 1;  // placement through smem lists
-    using Out = TOut<MAXC>;
+    constexpr bool kGen = gen_children_of<T>::value;  // children described by a generator (N-Queens)
+    using Out = TOut<kGen ? 1 : MAXC>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
 
     const uint32_t lane = threadIdx.x & 31u;
@@ -349,12 +358,13 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
             myfn = meta_fn(h.z);
             T::exec(args, meta_fn(h.z), meta_state(h.z), d, o, bx);
             if (o.action == 0u) o.err = GTAP_E_BAD_STATE;
-            if (NQ > 1) {  // queue(expr) out of range is a usage error
+            if (NQ > 1 && !kGen) {  // queue(expr) out of range is a usage error
                 if (o.action == Out::kSuspend && o.next_queue >= (uint32_t)NQ) o.err = GTAP_E_INVAL;
 #pragma unroll
                 for (int c = 0; c < MAXC; ++c)
                     if ((uint32_t)c < o.nchild && o.cq[c] >= (uint32_t)NQ) o.err = GTAP_E_INVAL;
             }
+            if (kGen && o.nchild > (uint32_t)MAXC) o.err = GTAP_E_CHILD_LIMIT;
         }
         __syncwarp();
         uint32_t err = o.err;
@@ -413,11 +423,18 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
                 const uint32_t g = excl + c;
                 cid[c] = (g < fromF) ? sm.fbuf[g] : sm.abuf[g - fromF];
                 TaskRec* cr = p.rec + cid[c];
-                st_v4(cr, make_uint4(0u, 0u, make_meta(o.cfn[c], 0, c, o.cq[c]), T::kTaskwait ? my : kNone));
-                st_v4(&cr->d[0], make_uint4(o.cd[c][0], o.cd[c][1], o.cd[c][2], o.cd[c][3]));
+                uint32_t cfn, cq, cd[kDataWords];
+                if constexpr (kGen) {
+                    T::gen_child(o.gen, o.gmask, (uint32_t)c, cfn, cq, cd);
+                } else {
+                    cfn = o.cfn[c]; cq = o.cq[c];
+                    cd[0] = o.cd[c][0]; cd[1] = o.cd[c][1]; cd[2] = o.cd[c][2]; cd[3] = o.cd[c][3];
+                }
+                st_v4(cr, make_uint4(0u, 0u, make_meta(cfn, 0, c, cq), T::kTaskwait ? my : kNone));
+                st_v4(&cr->d[0], make_uint4(cd[0], cd[1], cd[2], cd[3]));
                 if constexpr (kGeneric) {
-                    sm.cbuf[g] = cid[c] | (task_is_heavy<T>(o.cfn[c], o.cd[c]) ? kHeavyBit : 0u);
-                    sm.cqb[g] = (uint8_t)o.cq[c];
+                    sm.cbuf[g] = cid[c] | (task_is_heavy<T>(cfn, cd) ? kHeavyBit : 0u);
+                    sm.cqb[g] = (uint8_t)cq;
                 }
             }
         }

@@ -62,7 +62,7 @@ class Stats(ctypes.Structure):
 EXPORTS = [
     "gtap_abi_version", "gtap_status_str", "gtap_config_default", "gtap_workspace_bytes", "gtap_init",
     "gtap_spawn_root", "gtap_reset", "gtap_run", "gtap_sync", "gtap_root_result", "gtap_finalize",
-    "gtap_geometry", "gtap_table_destroy", "gtap_table_fib", "gtap_table_fib_cutoff", "gtap_table_mergesort",
+    "gtap_geometry", "gtap_table_destroy", "gtap_table_fib", "gtap_table_fib_cutoff", "gtap_table_nqueens", "gtap_table_mergesort",
     "gtap_table_spmv",
     "gtap_table_bfs", "gtap_bfs_init_depth", "gtap_ubench_atomics",
 ]
@@ -100,6 +100,8 @@ def lib():
     L.gtap_table_fib.restype = vp
     L.gtap_table_fib_cutoff.argtypes = [i32, u32]
     L.gtap_table_fib_cutoff.restype = vp
+    L.gtap_table_nqueens.argtypes = [i32, i32, vp]
+    L.gtap_table_nqueens.restype = vp
     L.gtap_table_mergesort.argtypes = [vp, vp, u64, i32]
     L.gtap_table_mergesort.restype = vp
     L.gtap_table_spmv.argtypes = [vp, vp, vp, vp, vp, u32, u32, u32]
@@ -161,6 +163,11 @@ class Table:
     def fib_cutoff(cutoff: int, num_queues: int = 1) -> "Table":
         """fib with a cutoff; num_queues=3 routes tasks with the paper's EPAQ classifier."""
         return Table(lib().gtap_table_fib_cutoff(cutoff, num_queues), "fib_cutoff", GTAP_WORKER_THREAD)
+
+    @staticmethod
+    def nqueens(n: int, cutoff: int, count) -> "Table":
+        """N-Queens; `count` is a CUDA int64 tensor of one element the run adds solutions to."""
+        return Table(lib().gtap_table_nqueens(n, cutoff, count.data_ptr()), "nqueens", GTAP_WORKER_THREAD, (count,))
 
     @staticmethod
     def mergesort(keys, scratch, cutoff: int = 128) -> "Table":

@@ -42,6 +42,8 @@ def lib():
         L.oracle_nqueens.argtypes = [ctypes.c_int32, ctypes.c_int32, i64p, i64p]
         L.oracle_nqueens.restype = ctypes.c_int
         L.oracle_mergesort.argtypes = [vp, vp, ctypes.c_int64, ctypes.c_int64, i64p, i64p]
+        L.oracle_cilksort.argtypes = [vp, vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, i64p, i64p]
+        L.oracle_cilksort.restype = ctypes.c_int
         L.oracle_spmv.argtypes = [vp, vp, vp, vp, ctypes.c_int64, vp, vp]
         L.oracle_bfs.argtypes = [vp, vp, ctypes.c_int64, ctypes.c_int32, vp]
         for f in (L.oracle_fib, L.oracle_mergesort, L.oracle_spmv, L.oracle_bfs):
@@ -95,6 +97,17 @@ def mergesort(keys, cutoff: int = 128):
     rc = lib().oracle_mergesort(_ptr(a), _ptr(tmp), a.size, cutoff, ctypes.byref(t), ctypes.byref(i))
     if rc != 0:
         raise ValueError("mergesort: bad arguments")
+    return a, t.value, i.value
+
+
+def cilksort(keys, cut_sort: int = 64, cut_merge: int = 256):
+    """(sorted copy, tasks, invocations) of Cilksort (parallel merge)."""
+    a = _np(keys, np.int32).copy()
+    tmp = np.empty_like(a)
+    t, i = ctypes.c_int64(), ctypes.c_int64()
+    rc = lib().oracle_cilksort(_ptr(a), _ptr(tmp), a.size, cut_sort, cut_merge, ctypes.byref(t), ctypes.byref(i))
+    if rc != 0:
+        raise ValueError("cilksort: bad arguments")
     return a, t.value, i.value
 
 

@@ -202,6 +202,103 @@ int oracle_mergesort(int32_t *data, int32_t *scratch, int64_t n, int64_t cutoff,
     return 0;
 }
 
+/* ------------------------------------------------------------- Cilksort */
+/*
+ * Cilksort (mergesort whose merge is parallelised;
+ * CUTOFF_SORT = 64, CUTOFF_MERGE = 256). Readings (R26):
+ *   sort(l, r): if r - l <= CUTOFF_SORT: insertion sort; else fork sort(l, m),
+ *               sort(m, r) with m = l + (r - l) / 2; join; fork merge of
+ *               [l, m) and [m, r) into the other buffer; join.
+ *   merge(A = [a0, a1) of the left run, B = [b0, b1) of the right run) writes
+ *               dst[a0 + b0 - m ...): if |A| + |B| <= CUTOFF_MERGE: two-pointer
+ *               merge (left first on ties); else split the longer run at its
+ *               middle element s and binary-search the other run (left run
+ *               split: B elements < A[s] go left; right run split: A elements
+ *               <= B[s] go left), fork both halves, join.
+ * Sorting happens in place in `data` (scratch holds the merged runs one level
+ * up: the oracle copies back after each merge so every level reads `data`).
+ * Counts: tasks and invocations (sort: 1 leaf / 3 internal; merge: 1 leaf /
+ * 2 internal).
+ */
+typedef struct { int64_t tasks, invocations; } cs_stats;
+
+static void cs_seq_merge(const int32_t *a, int64_t na, const int32_t *b, int64_t nb, int32_t *out)
+{
+    int64_t i = 0, j = 0, k = 0;
+    while (i < na && j < nb) out[k++] = (b[j] < a[i]) ? b[j++] : a[i++];
+    while (i < na) out[k++] = a[i++];
+    while (j < nb) out[k++] = b[j++];
+}
+
+static int64_t lower_bound_i32(const int32_t *p, int64_t lo, int64_t hi, int32_t v)
+{   /* first index in [lo, hi) with p[idx] >= v */
+    while (lo < hi) {
+        int64_t mid = lo + (hi - lo) / 2;
+        if (p[mid] < v) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+static int64_t upper_bound_i32(const int32_t *p, int64_t lo, int64_t hi, int32_t v)
+{   /* first index in [lo, hi) with p[idx] > v */
+    while (lo < hi) {
+        int64_t mid = lo + (hi - lo) / 2;
+        if (p[mid] <= v) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+static void cs_merge(const int32_t *src, int32_t *dst, int64_t m, int64_t a0, int64_t a1, int64_t b0, int64_t b1,
+                     int64_t cut_merge, cs_stats *st)
+{
+    st->tasks += 1;
+    const int64_t na = a1 - a0, nb = b1 - b0;
+    if (na + nb <= cut_merge) {
+        cs_seq_merge(src + a0, na, src + b0, nb, dst + (a0 + b0 - m));
+        st->invocations += 1;
+        return;
+    }
+    int64_t sa, sb;
+    if (na >= nb) {          /* split the left run at its middle */
+        sa = a0 + na / 2;
+        sb = lower_bound_i32(src, b0, b1, src[sa]);
+    } else {                 /* split the right run at its middle */
+        sb = b0 + nb / 2;
+        sa = upper_bound_i32(src, a0, a1, src[sb]);
+    }
+    cs_merge(src, dst, m, a0, sa, b0, sb, cut_merge, st);
+    cs_merge(src, dst, m, sa, a1, sb, b1, cut_merge, st);
+    st->invocations += 2;
+}
+
+static void cs_sort(int32_t *data, int32_t *tmp, int64_t l, int64_t r, int64_t cut_sort, int64_t cut_merge,
+                    cs_stats *st)
+{
+    st->tasks += 1;
+    if (r - l <= cut_sort) {
+        insertion_sort(data, l, r);
+        st->invocations += 1;
+        return;
+    }
+    const int64_t m = l + (r - l) / 2;
+    cs_sort(data, tmp, l, m, cut_sort, cut_merge, st);
+    cs_sort(data, tmp, m, r, cut_sort, cut_merge, st);
+    cs_merge(data, tmp, m, l, m, m, r, cut_merge, st);   /* into tmp[l, r) */
+    memcpy(data + l, tmp + l, (size_t)(r - l) * sizeof(int32_t));
+    st->invocations += 3;
+}
+
+int oracle_cilksort(int32_t *data, int32_t *scratch, int64_t n, int64_t cut_sort, int64_t cut_merge,
+                    int64_t *tasks, int64_t *invocations)
+{
+    if (n < 0 || cut_sort < 1 || cut_merge < 2) return -1;
+    cs_stats st = {0, 0};
+    cs_sort(data, scratch, 0, n, cut_sort, cut_merge, &st);
+    *tasks = st.tasks;
+    *invocations = st.invocations;
+    return 0;
+}
+
 /* ----------------------------------------------------------------- SpMV */
 /*
  * SpMV is only named by the paper as a block-cooperative workload (P:42,

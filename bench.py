@@ -43,6 +43,7 @@ SPMV_ROWS = 1 << 22
 SPMV_NNZ_CUT = 8192
 SPMV_FANOUT = 32
 SPMV_CFG = dict(grid_size=148 * 8, block_size=128, max_tasks_per_worker=1024)
+CS_CFG = dict(grid_size=0, block_size=128, max_tasks_per_worker=4096)
 NQ_N = 16
 NQ_CUTOFF = 7
 NQ_CFG = dict(grid_size=0, block_size=128, max_tasks_per_worker=4096)
@@ -281,6 +282,35 @@ def bench_epaq(dev, cutoff=10, reps=3):
                 paper="~1.8x on GH200 (P:788)")
 
 
+def bench_cilksort(dev, reps=3):
+    """SURVEY §8(f) NEXT #2: Cilksort of the same 2^24 keys (parallel merge, P:467)."""
+    import torch
+
+    import synth
+    import paper_2604_05982_b200 as g
+    pristine = synth.keys_int32(MS_N, seed=42, device=dev)
+    keys = torch.empty_like(pristine)
+    scratch = torch.empty_like(pristine)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
+    with g.Runtime(g.GTAP_WORKER_THREAD, dev.index, **CS_CFG) as rt:
+        ms = []
+        for i in range(reps + 1):
+            keys.copy_(pristine)
+            flush.fill_(1)
+            st = g.cilksort_(keys, scratch, 64, 256, rt=rt)
+            if i:
+                ms.append(st.device_ms)
+    ok = bool(torch.all(keys[1:] >= keys[:-1]).item())
+    t = statistics.median(ms)
+    pk, _ = peaks()
+    levels = _ms_levels(MS_N, 64)
+    algo = 8.0 * MS_N * (1 + levels)
+    return dict(workload="Cilksort 2^24 int32, cut 64/256 (NEXT #2), thread-level", metric="Mkeys/s",
+                value=MS_N / (t * 1e-3) / 1e6, ms=t, tasks=st.tasks, sorted=ok,
+                roofline=dict(bound="hbm", achieved=algo / (t * 1e-3) / 1e9, peak=pk["hbm_gbs"], unit="GB/s",
+                              frac=algo / (t * 1e-3) / 1e9 / pk["hbm_gbs"]))
+
+
 def bench_nqueens(dev, reps=3):
     """SURVEY §8(f) NEXT #4: N-Queens n = 16, cutoff depth 7 (P:465, P:588)."""
     import paper_2604_05982_b200 as g
@@ -411,6 +441,7 @@ def run_ours(args):
             secondary.append(dict(workload="L2 atomic probes", metric="ops/s", value=atoms))
             secondary.append(bench_epaq(dev))
             secondary.append(bench_nqueens(dev))
+            secondary.append(bench_cilksort(dev))
         except Exception as e:  # secondary results must not kill the main line
             secondary.append(dict(workload="fib40/atomics", error=repr(e)))
         try:

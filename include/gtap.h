@@ -195,6 +195,13 @@ const gtap_task_table *gtap_table_nqueens(int32_t n, int32_t cutoff, unsigned lo
 const gtap_task_table *gtap_table_mergesort(int32_t *keys, int32_t *scratch, uint64_t n,
                                             int32_t cutoff);
 
+/* Cilksort: mergesort whose merge is fork-join (split the
+ * longer run at its middle, binary-search the other). keys/scratch: int32[n]
+ * device buffers, n < 2^25; cut_sort in [1, 256], cut_merge >= 2 (paper: 64 /
+ * 256). Output sorted in keys. fn 0, root args {uint32 l, uint32 r}. */
+const gtap_task_table *gtap_table_cilksort(int32_t *keys, int32_t *scratch, uint64_t n, int32_t cut_sort,
+                                           int32_t cut_merge);
+
 /* SpMV y = A x over CSR (P:42 names SpMV as block-cooperative), block-level,
  * no taskwait. Task spmv(lo, hi) splits the row range into `fanout` equal
  * parts while it holds more than nnz_cut non-zeros (and > 1 row); leaves are

@@ -17,7 +17,7 @@ from . import gtap
 from .gtap import (GTAP_WORKER_BLOCK, GTAP_WORKER_THREAD, GtapError, Runtime, RunStats, Table,
                    bfs_init_depth, ubench_atomics)
 
-__all__ = ["gtap", "Runtime", "Table", "RunStats", "GtapError", "fib", "fib_cutoff", "nqueens", "mergesort_", "mergesort_forest_",
+__all__ = ["gtap", "Runtime", "Table", "RunStats", "GtapError", "fib", "fib_cutoff", "nqueens", "mergesort_", "cilksort_", "mergesort_forest_",
            "spmv", "bfs", "ubench_atomics", "GTAP_WORKER_THREAD", "GTAP_WORKER_BLOCK"]
 
 
@@ -83,6 +83,24 @@ def mergesort_(keys, scratch=None, cutoff: int = 128, rt: Runtime | None = None,
         scratch = torch.empty_like(keys)
     rt, own = _runtime(GTAP_WORKER_THREAD, rt, keys.device.index or 0, cfg)
     table = Table.mergesort(keys, scratch, cutoff)
+    try:
+        rt.spawn_root(table, (0, keys.numel()))
+        rt.run(stream)
+        return rt.sync()
+    finally:
+        table.close()
+        if own:
+            rt.close()
+
+
+def cilksort_(keys, scratch=None, cut_sort: int = 64, cut_merge: int = 256, rt: Runtime | None = None, stream=None,
+              **cfg):
+    """Sort a CUDA int32 tensor in place with Cilksort (parallel merge)."""
+    import torch
+    if scratch is None:
+        scratch = torch.empty_like(keys)
+    rt, own = _runtime(GTAP_WORKER_THREAD, rt, keys.device.index or 0, cfg)
+    table = Table.cilksort(keys, scratch, cut_sort, cut_merge)
     try:
         rt.spawn_root(table, (0, keys.numel()))
         rt.run(stream)

@@ -25,7 +25,7 @@ def build(force: bool = False) -> str:
     """Compile oracle.c -> liboracle.so (gcc -O2, single thread)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         tmp = _LIB + f".{os.getpid()}.tmp"
-        subprocess.check_call(["gcc", "-O2", "-std=c11", "-shared", "-fPIC", "-o", tmp, _SRC])
+        subprocess.check_call(["gcc", "-O2", "-std=gnu11", "-ffp-contract=off", "-shared", "-fPIC", "-o", tmp, _SRC, "-lm"])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -39,6 +39,10 @@ def lib():
         L.oracle_fib.argtypes = [ctypes.c_int32, i64p, i64p, i64p]
         L.oracle_fib_cutoff.argtypes = [ctypes.c_int32, ctypes.c_int32, i64p, i64p, i64p, i64p]
         L.oracle_fib_cutoff.restype = ctypes.c_int
+        L.oracle_tree.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint64, vp,
+                                  ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64,
+                                  ctypes.POINTER(ctypes.c_uint64), i64p]
+        L.oracle_tree.restype = ctypes.c_int
         L.oracle_nqueens.argtypes = [ctypes.c_int32, ctypes.c_int32, i64p, i64p]
         L.oracle_nqueens.restype = ctypes.c_int
         L.oracle_mergesort.argtypes = [vp, vp, ctypes.c_int64, ctypes.c_int64, i64p, i64p]
@@ -79,6 +83,17 @@ def fib_cutoff(n: int, cutoff: int):
     if rc != 0:
         raise ValueError(f"fib_cutoff: bad arguments n={n} cutoff={cutoff}")
     return v.value, t.value, i.value, c.value
+
+
+def tree(D: int, buf, mem_ops: int, compute_iters: int, pruned: bool = False, B: int = 3, seed: int = 1):
+    """(sum of do_memory_and_compute over all nodes mod 2^64, tasks) of the synthetic tree."""
+    b = _np(buf, np.uint64)
+    tot, t = ctypes.c_uint64(), ctypes.c_int64()
+    rc = lib().oracle_tree(D, B, 1 if pruned else 0, seed, _ptr(b), b.size, mem_ops, compute_iters,
+                           ctypes.byref(tot), ctypes.byref(t))
+    if rc != 0:
+        raise ValueError("tree: bad arguments")
+    return tot.value, t.value
 
 
 def nqueens(n: int, cutoff: int = 7):

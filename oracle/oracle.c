@@ -19,6 +19,7 @@
  *   bfs        -- all-pairs shortest paths (scipy) on every 5-vertex graph,
  *                 Graph500-style validity on RMAT graphs
  */
+#include <math.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -88,6 +89,89 @@ int oracle_fib_cutoff(int32_t n, int32_t cutoff, int64_t *value, int64_t *tasks,
     if (n < 0 || n > 92 || cutoff < 0) return -1;
     *tasks = *invocations = *serial_calls = 0;
     *value = fib_cut_rec(n, cutoff, tasks, invocations, serial_calls);
+    return 0;
+}
+
+/* ------------------------------------------------------- synthetic trees */
+/*
+ * Synthetic tree benchmark (§6.3): "Each node in a tree
+ * corresponds to one task. A task spawns child tasks (if any), performs
+ * taskwait, and then executes do_memory_and_compute"; the work is
+ * `mem_ops` pseudo-random 64-bit global loads and `compute_iters` FP64 FMAs
+ * (P:611). Full binary tree of depth D: 2^(D+1) - 1 tasks. Pruned
+ * B-ary tree (B = 3): at depth d each child is generated with probability
+ * p(d) = 1 - d/D. Readings (R27):
+ *   - node ids: full tree heap ids (root 1, children 2i, 2i+1); B-ary ids
+ *     (root 0, children B*i + 1 + k); a child exists iff
+ *     mix(seed ^ child_id) >> 11 < floor((D - d) * 2^53 / D) (counter-based:
+ *     the shape does not depend on the schedule);
+ *   - do_memory_and_compute(id) = sum_i buf[mix(id * G + i) mod len]
+ *     + sum over 32 independent FMA chains of the final chain value's bits
+ *     (chain c: f = 1 + ((id + c) & 1023) / 1024, then f = fma(f, 0.999999, 1e-7)
+ *     repeated compute_iters / 32 (+1 for c < compute_iters mod 32) times),
+ *     all mod 2^64; the run's value is the sum over all nodes.
+ */
+static uint64_t t_mix(uint64_t z)
+{
+    z ^= z >> 30; z *= 0xBF58476D1CE4E5B9ull;
+    z ^= z >> 27; z *= 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+static uint64_t tree_work(uint64_t id, const uint64_t *buf, uint64_t len, int64_t mem_ops, int64_t compute_iters)
+{
+    uint64_t s = 0;
+    for (int64_t i = 0; i < mem_ops; i++)
+        s += buf[t_mix(id * 0x9E3779B97F4A7C15ull + (uint64_t)i) % len];
+    for (int c = 0; c < 32; c++) {
+        double f = 1.0 + (double)((id + (uint64_t)c) & 1023u) / 1024.0;
+        int64_t it = compute_iters / 32 + (c < compute_iters % 32 ? 1 : 0);
+        for (int64_t j = 0; j < it; j++) f = fma(f, 0.999999, 1e-7);
+        uint64_t bits;
+        memcpy(&bits, &f, 8);
+        s += bits;
+    }
+    return s;
+}
+
+typedef struct {
+    const uint64_t *buf; uint64_t len; int64_t mem_ops, compute_iters;
+    int32_t D, B, pruned; uint64_t seed;
+    uint64_t total; int64_t tasks;
+} tree_ctx;
+
+static int tree_child_exists(const tree_ctx *t, uint64_t child, int32_t depth)
+{   /* depth = the parent's depth d; p(d) = 1 - d/D */
+    const uint64_t thr = (uint64_t)(((unsigned __int128)(uint64_t)(t->D - depth) << 53) / (uint64_t)t->D);
+    return (t_mix(t->seed ^ child) >> 11) < thr;
+}
+
+static void tree_node(tree_ctx *t, uint64_t id, int32_t depth)
+{
+    t->tasks += 1;
+    if (depth < t->D) {
+        if (!t->pruned) {
+            tree_node(t, 2 * id, depth + 1);
+            tree_node(t, 2 * id + 1, depth + 1);
+        } else {
+            for (int k = 0; k < t->B; k++) {
+                const uint64_t c = (uint64_t)t->B * id + 1 + (uint64_t)k;
+                if (tree_child_exists(t, c, depth)) tree_node(t, c, depth + 1);
+            }
+        }
+    }
+    t->total += tree_work(id, t->buf, t->len, t->mem_ops, t->compute_iters);  /* after the join */
+}
+
+int oracle_tree(int32_t D, int32_t B, int32_t pruned, uint64_t seed, const uint64_t *buf, uint64_t len,
+                int64_t mem_ops, int64_t compute_iters, uint64_t *total, int64_t *tasks)
+{
+    if (D < 0 || D > 40 || len == 0 || mem_ops < 0 || compute_iters < 0 || (pruned && (B < 1 || D < 1)))
+        return -1;
+    tree_ctx t = {buf, len, mem_ops, compute_iters, D, B, pruned, seed, 0, 0};
+    tree_node(&t, pruned ? 0 : 1, 0);
+    *total = t.total;
+    *tasks = t.tasks;
     return 0;
 }
 

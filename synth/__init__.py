@@ -27,7 +27,7 @@ import torch
 
 __all__ = [
     "mix64", "counter_u64", "uniform01_f64",
-    "keys_int32", "powerlaw_csr", "rmat_csr", "bfs_sources", "stream_key",
+    "keys_int32", "powerlaw_csr", "rmat_csr", "bfs_sources", "stream_key", "tree_buffer",
 ]
 
 _GAMMA = 0x9E3779B97F4A7C15
@@ -115,6 +115,13 @@ def powerlaw_csr(nrows: int, ncols: int | None = None, seed: int = 7, xm: int = 
     x = (0.5 + _srl(counter_u64(stream_key(seed, 14), _arange(ncols, device)), 41)
          .to(torch.float64) * (2.0 ** -23)).to(torch.float32)
     return row_ptr.to(torch.int32), col, val, x
+
+
+# ----------------------------------------------------------- synthetic tree
+
+def tree_buffer(n_words: int, seed: int = 9, device="cpu") -> torch.Tensor:
+    """n_words pseudo-random 64-bit words (the table do_memory_and_compute reads)."""
+    return counter_u64(stream_key(seed, 300), _arange(n_words, device))
 
 
 # ----------------------------------------------------------------------- BFS

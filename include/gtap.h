@@ -188,6 +188,25 @@ const gtap_task_table *gtap_table_fib_cutoff(int32_t cutoff, uint32_t num_queues
  * receives the number of solutions. fn 0, root args {} (nbytes 0). */
 const gtap_task_table *gtap_table_nqueens(int32_t n, int32_t cutoff, unsigned long long *d_count);
 
+/* Synthetic tree (§6.3), on either worker kind
+ * (worker_kind = GTAP_WORKER_THREAD: one task per lane; GTAP_WORKER_BLOCK: the
+ * body runs data-parallel over the block). A node spawns its children, joins
+ * (taskwait), then runs do_memory_and_compute.
+ * B = 0: full binary tree of depth D (2^(D+1) - 1 tasks), root args
+ *        {id lo = 1, id hi = 0, depth = 0}; children of id are 2id, 2id+1.
+ * B in [1, 8]: pruned B-ary tree, root args {0, 0, 0}; child k of id at
+ *        depth d is B*id + 1 + k, kept iff mix(seed ^ child) >> 11 <
+ *        floor((D - d) * 2^53 / D) (p(d) = 1 - d/D; R27); D >= 1.
+ * do_memory_and_compute(id): mem_ops 64-bit loads of buf[mix(id * G + i) & (len-1)]
+ * and compute_iters FP64 FMAs in min(64, compute_iters) chains, summed with the
+ * chains' final bits mod 2^64 (R27). buf: device uint64[len], len a power of
+ * two, read-only; d_total: caller-owned device uint64[32], zeroed by the
+ * caller; the run's value is the sum of the 32 words mod 2^64. D in [0, 40].
+ * NULL on bad arguments. */
+const gtap_task_table *gtap_table_tree(int32_t worker_kind, int32_t D, int32_t B, uint64_t seed,
+                                       const unsigned long long *buf, uint64_t len, uint32_t mem_ops,
+                                       uint32_t compute_iters, unsigned long long *d_total);
+
 /* mergesort with cutoff (state machine P:59-74), thread-level.
  * keys: int32[n] device buffer sorted in place; scratch: int32[n] device
  * buffer (ping-pong target); cutoff in [1, 256]. fn 0, root args

@@ -8,6 +8,8 @@ fails loudly when the library or the GPU is missing -- there is no CPU path):
     mergesort_forest_(keys, seg) -> stats              independent roots (forest)
     spmv(row_ptr, col, val, x)   -> (y, stats)         block-level, P:42
     bfs(row_ptr, col, src)       -> (depth, stats)     block-level, P:1053-1068
+    tree(D, buf, mem, comp)      -> (sum, stats)       thread- or block-level, P:604-675
+    nqueens(n) / cilksort_(keys) / fib_cutoff(n, c)    NEXT rows
 
 Lower level: gtap.Runtime / gtap.Table mirror include/gtap.h one to one.
 """
@@ -17,7 +19,7 @@ from . import gtap
 from .gtap import (GTAP_WORKER_BLOCK, GTAP_WORKER_THREAD, GtapError, Runtime, RunStats, Table,
                    bfs_init_depth, ubench_atomics)
 
-__all__ = ["gtap", "Runtime", "Table", "RunStats", "GtapError", "fib", "fib_cutoff", "nqueens", "mergesort_", "cilksort_", "mergesort_forest_",
+__all__ = ["gtap", "Runtime", "Table", "RunStats", "GtapError", "fib", "fib_cutoff", "nqueens", "tree", "mergesort_", "cilksort_", "mergesort_forest_",
            "spmv", "bfs", "ubench_atomics", "GTAP_WORKER_THREAD", "GTAP_WORKER_BLOCK"]
 
 
@@ -70,6 +72,27 @@ def nqueens(n: int, cutoff: int = 7, rt: Runtime | None = None, device: int = 0,
         rt.run(stream)
         st = rt.sync()
         return int(count.item()), st
+    finally:
+        table.close()
+        if own:
+            rt.close()
+
+
+def tree(D: int, buf, mem_ops: int, compute_iters: int, pruned: bool = False, B: int = 3, seed: int = 1,
+         worker: int = GTAP_WORKER_THREAD, rt: Runtime | None = None, stream=None, **cfg):
+    """Synthetic tree on thread- or block-level workers.
+
+    Returns (sum of do_memory_and_compute over all nodes mod 2^64, stats); buf: CUDA int64 tensor of
+    power-of-two length (the words the pseudo-random loads read)."""
+    import torch
+    total = torch.zeros(32, dtype=torch.int64, device=buf.device)
+    rt, own = _runtime(worker, rt, buf.device.index or 0, cfg)
+    table = Table.tree(worker, D, B if pruned else 0, seed, buf, mem_ops, compute_iters, total)
+    try:
+        rt.spawn_root(table, (0 if pruned else 1, 0, 0))
+        rt.run(stream)
+        st = rt.sync()
+        return int(total.sum().item()) & ((1 << 64) - 1), st
     finally:
         table.close()
         if own:

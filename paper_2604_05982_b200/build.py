@@ -23,7 +23,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
          "--expt-relaxed-constexpr", "-I", INCLUDE, "-I", CSRC]
 SOURCES = ["runtime.cu", "table_fib.cu", "table_mergesort.cu", "table_spmv.cu", "table_bfs.cu", "table_nqueens.cu",
-           "table_cilksort.cu", "ubench.cu"]
+           "table_cilksort.cu", "table_tree.cu", "ubench.cu"]
 
 
 def _digest() -> str:

@@ -62,7 +62,7 @@ class Stats(ctypes.Structure):
 EXPORTS = [
     "gtap_abi_version", "gtap_status_str", "gtap_config_default", "gtap_workspace_bytes", "gtap_init",
     "gtap_spawn_root", "gtap_reset", "gtap_run", "gtap_sync", "gtap_root_result", "gtap_finalize",
-    "gtap_geometry", "gtap_table_destroy", "gtap_table_fib", "gtap_table_fib_cutoff", "gtap_table_nqueens", "gtap_table_mergesort", "gtap_table_cilksort",
+    "gtap_geometry", "gtap_table_destroy", "gtap_table_fib", "gtap_table_fib_cutoff", "gtap_table_nqueens", "gtap_table_tree", "gtap_table_mergesort", "gtap_table_cilksort",
     "gtap_table_spmv",
     "gtap_table_bfs", "gtap_bfs_init_depth", "gtap_ubench_atomics",
 ]
@@ -102,6 +102,9 @@ def lib():
     L.gtap_table_fib_cutoff.restype = vp
     L.gtap_table_nqueens.argtypes = [i32, i32, vp]
     L.gtap_table_nqueens.restype = vp
+    L.gtap_table_tree.argtypes = [i32, i32, i32, ctypes.c_uint64, vp, ctypes.c_uint64, ctypes.c_uint32,
+                                  ctypes.c_uint32, vp]
+    L.gtap_table_tree.restype = vp
     L.gtap_table_mergesort.argtypes = [vp, vp, u64, i32]
     L.gtap_table_mergesort.restype = vp
     L.gtap_table_cilksort.argtypes = [vp, vp, u64, i32, i32]
@@ -165,6 +168,20 @@ class Table:
     def fib_cutoff(cutoff: int, num_queues: int = 1) -> "Table":
         """fib with a cutoff; num_queues=3 routes tasks with the paper's EPAQ classifier."""
         return Table(lib().gtap_table_fib_cutoff(cutoff, num_queues), "fib_cutoff", GTAP_WORKER_THREAD)
+
+    @staticmethod
+    def tree(kind: int, D: int, B: int, seed: int, buf, mem_ops: int, compute_iters: int, total) -> "Table":
+        """Synthetic tree (B = 0: full binary; else pruned B-ary); buf: CUDA int64/uint64 tensor of
+        power-of-two length, total: CUDA int64 tensor of 32 zeros."""
+        import torch
+        for t, n in ((buf, "buf"), (total, "total")):
+            if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.int64 and t.is_contiguous()):
+                raise TypeError(f"{n} must be a contiguous CUDA int64 tensor")
+        if total.numel() < 32:
+            raise ValueError("total must hold 32 counters")
+        h = lib().gtap_table_tree(kind, D, B, seed & ((1 << 64) - 1), buf.data_ptr(), buf.numel(), mem_ops,
+                                  compute_iters, total.data_ptr())
+        return Table(h, f"tree_{'thread' if kind == GTAP_WORKER_THREAD else 'block'}", kind, (buf, total))
 
     @staticmethod
     def nqueens(n: int, cutoff: int, count) -> "Table":

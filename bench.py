@@ -326,6 +326,33 @@ def bench_nqueens(dev, reps=3):
                 value=st.tasks / (t * 1e-3), ms=t, tasks=st.tasks, solutions=sol)
 
 
+TREE_CFG = {"thread": dict(grid_size=0, block_size=128, max_tasks_per_worker=4096),
+            "block": dict(grid_size=148 * 32, block_size=32, max_tasks_per_worker=2048)}
+
+
+def bench_tree(dev, reps=3):
+    """synthetic trees on both worker kinds: full binary D = 22
+    (mem_ops 64, compute_iters 256) and pruned 3-ary D = 24 (mem_ops 64, compute_iters 32768); the
+    pseudo-random loads read a 256 MiB table (HBM, not L2)."""
+    import synth
+    import paper_2604_05982_b200 as g
+    buf = synth.tree_buffer(1 << 25, device=dev)
+    pts = {}
+    for kind, wk in (("thread", g.GTAP_WORKER_THREAD), ("block", g.GTAP_WORKER_BLOCK)):
+        with g.Runtime(wk, dev.index, **TREE_CFG[kind]) as rt:
+            for name, D, mem, comp, pruned in (("full_D22", 22, 64, 256, False),
+                                               ("pruned_D24_comp32768", 24, 64, 32768, True)):
+                ms = []
+                for i in range(reps + 1):
+                    _, st = g.tree(D, buf, mem, comp, pruned=pruned, worker=wk, rt=rt)
+                    if i:
+                        ms.append(st.device_ms)
+                t = statistics.median(ms)
+                pts[f"{name}_{kind}"] = dict(ms=t, tasks=st.tasks, tasks_per_s=st.tasks / (t * 1e-3))
+    return dict(workload="synthetic trees (NEXT #3), thread- vs block-level", metric="tasks/s",
+                configs={k: dict(v) for k, v in TREE_CFG.items()}, points=pts)
+
+
 def bench_atomics(dev):
     import torch
 
@@ -442,6 +469,7 @@ def run_ours(args):
             secondary.append(bench_epaq(dev))
             secondary.append(bench_nqueens(dev))
             secondary.append(bench_cilksort(dev))
+            secondary.append(bench_tree(dev))
         except Exception as e:  # secondary results must not kill the main line
             secondary.append(dict(workload="fib40/atomics", error=repr(e)))
         try:

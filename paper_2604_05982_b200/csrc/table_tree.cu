@@ -92,8 +92,15 @@ struct TreeThreadTable {
     __device__ __forceinline__ static unsigned long long work(const Args& a, unsigned long long id) {
         unsigned long long s = 0;
         const unsigned long long base = id * 0x9E3779B97F4A7C15ull;
-#pragma unroll 4
-        for (uint32_t i = 0; i < a.mem_ops; ++i) s += __ldg(&a.buf[tree_mix(base + i) & a.lmask]);
+        uint32_t i = 0;
+        for (; i + 8u <= a.mem_ops; i += 8u) {  // 8 independent loads in flight per lane
+            unsigned long long v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = __ldg(&a.buf[tree_mix(base + i + u) & a.lmask]);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) s += v[u];
+        }
+        for (; i < a.mem_ops; ++i) s += __ldg(&a.buf[tree_mix(base + i) & a.lmask]);
         const uint32_t ci = a.compute_iters, nch = min(64u, ci), per = ci / 64u, rem = ci % 64u;
         for (uint32_t c = 0; c < nch; c += 4) {
             double f0 = chain_init(id, c), f1 = chain_init(id, c + 1), f2 = chain_init(id, c + 2),
@@ -169,7 +176,15 @@ struct TreeBlockTable {
         // do_memory_and_compute, data-parallel: loads strided over the block, one FMA chain per thread
         unsigned long long s = 0;
         const unsigned long long base = id * 0x9E3779B97F4A7C15ull;
-        for (uint32_t i = tid; i < a.mem_ops; i += bd) s += __ldg(&a.buf[tree_mix(base + i) & a.lmask]);
+        uint32_t i = tid;
+        for (; i + 7u * bd < a.mem_ops; i += 8u * bd) {  // 8 independent loads in flight per thread
+            unsigned long long v[8];
+#pragma unroll
+            for (uint32_t u = 0; u < 8u; ++u) v[u] = __ldg(&a.buf[tree_mix(base + i + u * bd) & a.lmask]);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) s += v[u];
+        }
+        for (; i < a.mem_ops; i += bd) s += __ldg(&a.buf[tree_mix(base + i) & a.lmask]);
         const uint32_t ci = a.compute_iters, nch = min(64u, ci), per = ci / 64u, rem = ci % 64u;
         for (uint32_t c = tid; c < nch; c += bd) {
             double f = chain_init(id, c);

@@ -107,7 +107,8 @@ typedef struct {
     float    device_ms;        /* CUDA-event time of the persistent kernel */
     uint32_t grid_size;        /* launched grid */
     uint32_t block_size;       /* launched block */
-    uint32_t reserved[2];
+    uint32_t assists;          /* task bodies run by the whole warp (warp assist, tables with kAssist) */
+    uint32_t reserved;
 } gtap_stats;
 
 /* ---- lifecycle ---------------------------------------------------------- */
@@ -210,9 +211,20 @@ const gtap_task_table *gtap_table_tree(int32_t worker_kind, int32_t D, int32_t B
 /* mergesort with cutoff (state machine P:59-74), thread-level.
  * keys: int32[n] device buffer sorted in place; scratch: int32[n] device
  * buffer (ping-pong target); cutoff in [1, 256]. fn 0, root args
- * {uint32 l, uint32 r} (normally {0, n}); result 0. */
+ * {uint32 l, uint32 r} (normally {0, n}); result 0. Same as
+ * gtap_table_mergesort_ex(..., GTAP_MERGE_WARP). */
 const gtap_task_table *gtap_table_mergesort(int32_t *keys, int32_t *scratch, uint64_t n,
                                             int32_t cutoff);
+
+/* How a merge task body runs. GTAP_MERGE_THREAD: on the task's own
+ * lane (the paper's thread-level merge; merges >= 8192 keys stream
+ * through shared memory by TMA). GTAP_MERGE_WARP: merges >= 8192 keys are run
+ * by all 32 lanes of the task's warp after the cycle's bodies (merge-path
+ * slices); the task graph, task counts and the
+ * sorted output are identical. */
+enum { GTAP_MERGE_THREAD = 0, GTAP_MERGE_WARP = 1 };
+const gtap_task_table *gtap_table_mergesort_ex(int32_t *keys, int32_t *scratch, uint64_t n,
+                                               int32_t cutoff, uint32_t merge_mode);
 
 /* Cilksort: mergesort whose merge is fork-join (split the
  * longer run at its middle, binary-search the other). keys/scratch: int32[n]

@@ -99,13 +99,15 @@ def tree(D: int, buf, mem_ops: int, compute_iters: int, pruned: bool = False, B:
             rt.close()
 
 
-def mergesort_(keys, scratch=None, cutoff: int = 128, rt: Runtime | None = None, stream=None, **cfg):
-    """Sort a CUDA int32 tensor in place with the cutoff mergesort task program."""
+def mergesort_(keys, scratch=None, cutoff: int = 128, merge_mode: int = 1, rt: Runtime | None = None, stream=None,
+               **cfg):
+    """Sort a CUDA int32 tensor in place with the cutoff mergesort task program
+    (merge_mode 1: heavy merges run by the task's whole warp; 0: the paper's one-lane merge)."""
     import torch
     if scratch is None:
         scratch = torch.empty_like(keys)
     rt, own = _runtime(GTAP_WORKER_THREAD, rt, keys.device.index or 0, cfg)
-    table = Table.mergesort(keys, scratch, cutoff)
+    table = Table.mergesort(keys, scratch, cutoff, merge_mode)
     try:
         rt.spawn_root(table, (0, keys.numel()))
         rt.run(stream)
@@ -134,15 +136,15 @@ def cilksort_(keys, scratch=None, cut_sort: int = 64, cut_merge: int = 256, rt: 
             rt.close()
 
 
-def mergesort_forest_(keys, segments, scratch=None, cutoff: int = 128, rt: Runtime | None = None, stream=None,
-                      **cfg):
+def mergesort_forest_(keys, segments, scratch=None, cutoff: int = 128, merge_mode: int = 1, rt: Runtime | None = None,
+                      stream=None, **cfg):
     """Sort independent segments [(l, r), ...] of one CUDA int32 tensor: one root per segment."""
     import torch
     if scratch is None:
         scratch = torch.empty_like(keys)
     cfg.setdefault("max_roots", max(len(segments), 1))
     rt, own = _runtime(GTAP_WORKER_THREAD, rt, keys.device.index or 0, cfg)
-    table = Table.mergesort(keys, scratch, cutoff)
+    table = Table.mergesort(keys, scratch, cutoff, merge_mode)
     try:
         for l, r in segments:
             rt.spawn_root(table, (l, r))

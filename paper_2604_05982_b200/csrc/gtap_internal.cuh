@@ -76,7 +76,7 @@ struct __align__(64) FreeMeta {
 
 enum StatIdx : int {
     ST_TASKS = 0, ST_INVOC, ST_POPS, ST_KEPT, ST_STEALS_OK, ST_STEALS_FAILED, ST_STOLEN,
-    ST_PUSHES, ST_CYCLES, ST_IDLE, ST_REMOTE_FREES, ST_MAX_POOL, ST_COUNT = 16
+    ST_PUSHES, ST_CYCLES, ST_IDLE, ST_REMOTE_FREES, ST_MAX_POOL, ST_ASSISTS, ST_COUNT = 16
 };
 
 // Control block: each hot word on its own 128-B line.

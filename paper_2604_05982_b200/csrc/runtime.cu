@@ -343,6 +343,7 @@ gtap_status gtap_sync(gtap_runtime* rt, gtap_stats* out) {
         out->idle_cycles = c.stats[gtap::ST_IDLE];
         out->remote_frees = c.stats[gtap::ST_REMOTE_FREES];
         out->max_pool_used = c.stats[gtap::ST_MAX_POOL];
+        out->assists = (uint32_t)c.stats[gtap::ST_ASSISTS];
         out->error_word = c.error;
         out->workers = rt->run_W;
         out->device_ms = ms;

@@ -58,9 +58,17 @@ struct TOut {
     // generated children (tables with kGenChildren): child c is T::gen_child(gen, gmask, c, ...)
     uint32_t gen[kDataWords];
     uint32_t gmask;
+    // warp assist (tables with kAssist): the body's heavy leaf routine is run by the whole warp
+    // after this cycle's bodies, before the task's spawns/join/finish are processed
+    uint32_t assist;
+    uint32_t ap[kDataWords];
     static constexpr uint32_t kFinish = 1, kSuspend = 2;
     __device__ __forceinline__ void init() {
         action = 0; nchild = 0; has_result = 0; err = 0; result = 0; next_state = 0; next_queue = 0;
+        assist = 0;
+    }
+    __device__ __forceinline__ void request_assist(uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3) {
+        assist = 1; ap[0] = a0; ap[1] = a1; ap[2] = a2; ap[3] = a3;
     }
     // spawn child #i (i is a compile-time constant after inlining) into queue q
     __device__ __forceinline__ void spawn_q(int i, uint32_t q, uint32_t fn, uint32_t d0, uint32_t d1 = 0,
@@ -101,6 +109,11 @@ template <class T, class = void>
 struct gen_children_of { static constexpr bool value = false; };
 template <class T>
 struct gen_children_of<T, decltype((void)T::kGenChildren, void())> { static constexpr bool value = T::kGenChildren; };
+
+template <class T, class = void>
+struct assist_of { static constexpr bool value = false; };
+template <class T>
+struct assist_of<T, decltype((void)T::kAssist, void())> { static constexpr bool value = T::kAssist; };
 
 template <class T, class = void>
 struct num_queues_of { static constexpr int value = 1; };
@@ -175,7 +188,8 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
     uint32_t rng = hash32(p.seed * 0x9E3779B97F4A7C15ull + (unsigned long long)w * 32u + lane);
     uint32_t backoff = 32;
     unsigned long long st_tasks = 0, st_inv = 0, st_pops = 0, st_kept = 0, st_sok = 0, st_sfail = 0,
-                       st_stolen = 0, st_push = 0, st_cyc = 0, st_idle = 0, st_rfree = 0;
+                       st_stolen = 0, st_push = 0, st_cyc = 0, st_idle = 0, st_rfree = 0,
+                       st_assist = 0;
     const unsigned long long t0 = globaltimer();
     uint32_t cyc_u = 0;  // warp-uniform cycle counter (every lane increments it)
     bool failed = false;
@@ -204,6 +218,7 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
     }
 
     while (true) {
+        if constexpr (assist_of<T>::value) T::help(args, lane, bx);  // join the block's open assist, if any
         // ================= (1) acquire =================
         uint32_t n = nkept;
         uint32_t my = (lane < n) ? (sm.kept[lane] & ~kHeavyBit) : kNone;
@@ -365,6 +380,24 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
                     if ((uint32_t)c < o.nchild && o.cq[c] >= (uint32_t)NQ) o.err = GTAP_E_INVAL;
             }
             if (kGen && o.nchild > (uint32_t)MAXC) o.err = GTAP_E_CHILD_LIMIT;
+        }
+        if constexpr (assist_of<T>::value) {
+            // (2b) warp assist: lanes whose body deferred a heavy leaf routine get the whole warp,
+            // one request at a time (a B200 choice; the task graph and
+            // the result are unchanged). T::assist fences its writes and syncs the warp, so the
+            // requesting lane's join release below covers every lane's stores.
+            uint32_t req = __ballot_sync(0xffffffffu, my != kNone && o.assist != 0u && o.err == 0u);
+            while (req) {
+                const uint32_t src = (uint32_t)__ffs(req) - 1u;
+                req &= req - 1u;
+                uint32_t ap[kDataWords];
+#pragma unroll
+                for (int k = 0; k < kDataWords; ++k) ap[k] = __shfl_sync(0xffffffffu, o.ap[k], src);
+                const bool aok = T::assist(args, ap, lane, bx);
+                const uint32_t okm = __ballot_sync(0xffffffffu, aok);
+                if (lane == src && okm != 0xffffffffu) o.err = GTAP_E_BAD_STATE;
+                if (lane == 0) ++st_assist;
+            }
         }
         __syncwarp();
         uint32_t err = o.err;
@@ -676,6 +709,7 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
         atomicAdd(&s[ST_CYCLES], st_cyc);
         atomicAdd(&s[ST_IDLE], st_idle);
         atomicAdd(&s[ST_REMOTE_FREES], st_rfree);
+        if (st_assist) atomicAdd(&s[ST_ASSISTS], st_assist);
         atomicMax(&s[ST_MAX_POOL], (unsigned long long)bump);
     }
 }

@@ -184,12 +184,35 @@ struct MergeSlot {                           // placed 2 KB-aligned inside the b
     unsigned long long mbar[2 * kChains][2];
     uint32_t par[2 * kChains];               // mbarrier parity bits per input ring
 };
+// warp-assist merge tiles (GTAP_MERGE_WARP): per warp, one smem ring per input run
+constexpr int kWT = 256;                     // outputs per tile
+constexpr int kVT = kWT / 32;                // outputs per lane per tile
+constexpr int kWR = 1024;                    // keys per ring (window + 3 tiles of prefetch)
+struct WarpTiles {
+    int32_t a[kWR];
+    int32_t b[kWR];
+};
+constexpr int kMsWarps = 4;                  // kMaxThreads / 32
+constexpr size_t cmax(size_t x, size_t y) { return x > y ? x : y; }
 struct MergeSlotHolder {                     // BlockExtra: 2 KB of slack to align the slot
-    unsigned char raw[sizeof(MergeSlot) + 2048];
+    // the TMA slot (GTAP_MERGE_THREAD) and the warp tiles (GTAP_MERGE_WARP) share the space:
+    // a table uses one or the other
+    unsigned char raw[cmax(sizeof(MergeSlot) + 2048, sizeof(WarpTiles) * kMsWarps + 128)];
     uint32_t busy;
+    // block assist board (GTAP_MERGE_WARP, merges >= kBlockAssistMin): one open merge per block
+    struct Board {
+        uint32_t state;               // 0 free, 1 being set up, 2 open
+        uint32_t l, m, r, depth;
+        uint32_t next;                // next chunk to claim (>= nchunks: closed)
+        uint32_t nchunks, done;
+    } board;
     __device__ __forceinline__ MergeSlot* slot() {
         const uint32_t a = tma::sa(raw);
         return reinterpret_cast<MergeSlot*>(raw + ((2048u - (a & 2047u)) & 2047u));
+    }
+    __device__ __forceinline__ WarpTiles* tiles(uint32_t warp) {
+        const uint32_t a = tma::sa(raw);
+        return reinterpret_cast<WarpTiles*>(raw + ((128u - (a & 127u)) & 127u)) + warp;
     }
 };
 
@@ -534,6 +557,129 @@ __device__ __noinline__ bool ms_merge_tma(const int32_t* src, int32_t* dst, uint
     return ok;
 }
 
+// ---------------------------------------------------------------------------
+// Warp-assisted merge (B200 design): a heavy merge
+// task's body is run by all 32 lanes of its warp after the cycle's bodies (the
+// other lanes' own tasks have run by then). The output is produced in tiles of
+// kWT keys. Each input run streams through a per-warp shared-memory ring of kWR
+// keys, kept topped up by 4-byte cp.async copies in 128-key chunks (one commit
+// group per tile; top-ups trail pa + kWR by < 128 keys and a tile consumes
+// <= kWT keys of a run, so the window a tile reads was issued >= 2 tiles
+// earlier and `wait_group 1` suffices). Per tile, lane k finds the
+// start of its kVT outputs by a stable merge-path search in the rings and merges
+// them serially from shared memory; the run consumption of the tile is the last
+// active lane's position. Ties take the left run first (search and serial step
+// alike), so the output is the stable two-pointer merge.
+namespace wm {
+__device__ __forceinline__ void cp4(const int32_t* sdst, const int32_t* gsrc) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(tma::sa(sdst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+// lanes copy src[from, to) into ring positions (global index & (kWR - 1)): whole 128-key chunks
+// (4 copies per lane, no tail) while they fit, the rest only at the run's end. Returns the new `from`.
+__device__ __forceinline__ uint32_t topup(int32_t* ring, const int32_t* src, uint32_t from, uint32_t to,
+                                          uint32_t end, uint32_t lane) {
+    while (from + 128u <= to) {
+#pragma unroll
+        for (uint32_t k = 0; k < 4u; ++k) {
+            const uint32_t i = from + lane + 32u * k;
+            cp4(ring + (i & (kWR - 1u)), src + i);
+        }
+        from += 128u;
+    }
+    if (to == end) {
+        for (uint32_t i = from + lane; i < to; i += 32u) cp4(ring + (i & (kWR - 1u)), src + i);
+        from = to;
+    }
+    return from;
+}
+}  // namespace wm
+
+// all 32 lanes: stable merge of src[a0, m) and src[b0, r) into dst[o0, o0 + (m - a0) + (r - b0))
+__device__ __noinline__ void warp_merge(const int32_t* __restrict__ src, int32_t* __restrict__ dst, uint32_t a0,
+                                        uint32_t m, uint32_t b0, uint32_t r, uint32_t o0, uint32_t lane,
+                                        WarpTiles* T) {
+    int32_t* RA = T->a;
+    int32_t* RB = T->b;
+    const uint32_t l = a0, oend = o0 + (m - a0) + (r - b0);
+    uint32_t pa = a0, pb = b0, out = o0;              // next key of each run, next output
+    uint32_t la = wm::topup(RA, src, l, min(m, l + (uint32_t)kWR), m, lane);   // loaded (issued) up to
+    uint32_t lb = wm::topup(RB, src, b0, min(r, b0 + (uint32_t)kWR), r, lane);
+    wm::commit();
+    wm::commit();
+    wm::commit();
+    while (out < oend) {
+        const uint32_t tile = min((uint32_t)kWT, oend - out);
+        wm::wait<1>();  // the window was issued >= 2 tiles ago (top-ups trail pa + kWR by < 128 keys)
+        __syncwarp();
+        const uint32_t na = min(tile, m - pa), nb = min(tile, r - pb);
+        const uint32_t d = min(lane * (uint32_t)kVT, tile);
+        uint32_t lo = d > nb ? d - nb : 0u, hi = min(d, na);
+        // stable merge-path split at diagonal d: the smallest i in [lo, hi] with !(A[i] <= B[d-1-i]);
+        // three probes per step (4-way), so ~4 dependent shared-memory round trips per tile
+        const uint32_t cb = pb + d - 1u;
+        while (lo < hi) {
+            const uint32_t w = hi - lo;
+            const uint32_t q1 = lo + (w >> 2), q2 = lo + (w >> 1), q3 = lo + ((3u * w) >> 2);
+            const bool p1 = RA[(pa + q1) & (kWR - 1u)] <= RB[(cb - q1) & (kWR - 1u)];
+            const bool p2 = RA[(pa + q2) & (kWR - 1u)] <= RB[(cb - q2) & (kWR - 1u)];
+            const bool p3 = RA[(pa + q3) & (kWR - 1u)] <= RB[(cb - q3) & (kWR - 1u)];
+            if (p3)      { lo = q3 + 1u; }
+            else if (p2) { lo = q2 + 1u; hi = q3; }
+            else if (p1) { lo = q1 + 1u; hi = q2; }
+            else         { hi = q1; }
+        }
+        uint32_t ai = lo, bi = d - lo;
+        const uint32_t cnt = min((uint32_t)kVT, tile - d);
+        int32_t va = RA[(pa + ai) & (kWR - 1u)], vb = RB[(pb + bi) & (kWR - 1u)];
+#pragma unroll
+        for (int v = 0; v < kVT; ++v) {
+            if ((uint32_t)v < cnt) {
+                const bool takeA = bi >= nb || (ai < na && !(vb < va));
+                dst[out + d + v] = takeA ? va : vb;
+                if (takeA) { ++ai; va = RA[(pa + ai) & (kWR - 1u)]; }
+                else       { ++bi; vb = RB[(pb + bi) & (kWR - 1u)]; }
+            }
+        }
+        const uint32_t ca = __shfl_sync(0xffffffffu, ai, (tile - 1u) / (uint32_t)kVT);  // A keys consumed
+        __syncwarp();                                  // ring reads done before the top-up
+        pa += ca;
+        pb += tile - ca;
+        out += tile;
+        la = wm::topup(RA, src, la, min(m, pa + (uint32_t)kWR), m, lane);
+        lb = wm::topup(RB, src, lb, min(r, pb + (uint32_t)kWR), r, lane);
+        wm::commit();
+    }
+    wm::wait<0>();
+    __threadfence();  // every lane's stores before the requesting lane's join release
+    __syncwarp();
+}
+
+// all 32 lanes: stable merge-path split (A keys among the first t outputs of merge(src[l, m), src[m, r)))
+// over global memory, 32 probes per step (a ~33-way search: ~5 dependent round trips for 2^23 keys)
+__device__ __noinline__ uint32_t warp_split(const int32_t* src, uint32_t l, uint32_t m, uint32_t r, uint32_t t,
+                                            uint32_t lane) {
+    uint32_t lo = t > (r - m) ? t - (r - m) : 0u, hi = min(t, m - l);
+    while (hi - lo > 32u) {
+        const uint32_t w = hi - lo;
+        const uint32_t q = lo + (uint32_t)(((unsigned long long)(lane + 1u) * w) / 33u);
+        const bool pr = __ldcg(src + l + q) <= __ldcg(src + m + (t - q - 1u));
+        const uint32_t cnt = (uint32_t)__popc(__ballot_sync(0xffffffffu, pr));  // trues form a prefix
+        const uint32_t qlo = __shfl_sync(0xffffffffu, q, (cnt + 31u) & 31u);
+        const uint32_t qhi = __shfl_sync(0xffffffffu, q, cnt & 31u);
+        if (cnt > 0u) lo = qlo + 1u;
+        if (cnt < 32u) hi = qhi;
+    }
+    const uint32_t q = lo + lane;
+    const bool pr = q < hi && __ldcg(src + l + q) <= __ldcg(src + m + (t - q - 1u));
+    return lo + (uint32_t)__popc(__ballot_sync(0xffffffffu, pr));
+}
+
+constexpr uint32_t kBlockAssistMin = 1u << 17;  // merges this long are shared by the block's warps
+constexpr uint32_t kChunk = 1u << 16;           // output keys per claimed chunk
+
 struct MergesortTable {
     static constexpr uint32_t kKind = GTAP_WORKER_THREAD;
     static constexpr int kMaxChildren = 2;
@@ -548,12 +694,80 @@ struct MergesortTable {
         return 2u * (d[1] - d[0]) >= kTmaMin;
     }
     static constexpr int kMaxThreads = 128, kMinBlocks = 4;  // __launch_bounds__: 128 regs, no spills
+    static constexpr bool kAssist = true;                    // heavy merges: warp assist (merge_mode 1)
+    static constexpr uint32_t kAssistMin = 8192;
     struct Args {
         int32_t* keys;
         int32_t* scratch;
         uint32_t cutoff;
         uint32_t n;         // array length (TMA path needs n % 4 == 0 and 16-B aligned buffers)
+        uint32_t mode;      // GTAP_MERGE_THREAD (0) or GTAP_MERGE_WARP (1)
+        uint32_t pad;
     };
+    // warp assist: ap = {l, r, depth}; all 32 lanes
+    __device__ __forceinline__ static bool assist(const Args& a, const uint32_t (&ap)[kDataWords], uint32_t lane,
+                                                  MergeSlotHolder* H) {
+        static_assert(kMaxThreads / 32 <= kMsWarps, "one WarpTiles per warp");
+        const uint32_t l = ap[0], r = ap[1], depth = ap[2];
+        const uint32_t m = l + (r - l) / 2u;
+        WarpTiles* T = H->tiles(threadIdx.x >> 5);
+        if (r - l >= kBlockAssistMin) {
+            // block assist: open the board, merge chunks alongside the block's other warps (they
+            // join at the top of their scheduler loops), wait until every chunk is done
+            volatile MergeSlotHolder::Board& B = H->board;
+            uint32_t got = 0;
+            if (lane == 0) got = (atomicCAS(&H->board.state, 0u, 1u) == 0u) ? 1u : 0u;
+            if (__shfl_sync(0xffffffffu, got, 0)) {
+                const uint32_t nch = (r - l + kChunk - 1u) / kChunk;
+                if (lane == 0) {
+                    B.l = l; B.m = m; B.r = r; B.depth = depth; B.nchunks = nch; B.done = 0u;
+                    __threadfence_block();
+                    atomicExch(&H->board.next, 0u);   // claims from here on see the parameters above
+                    __threadfence_block();
+                    B.state = 2u;
+                }
+                __syncwarp();
+                help_chunks(a, H, lane, T);
+                if (lane == 0) {
+                    while (B.done < nch) __nanosleep(128);
+                    atomicExch(&H->board.next, 0x80000000u);  // late claims see a closed board
+                    __threadfence_block();
+                    B.state = 0u;
+                }
+                __syncwarp();
+                __threadfence();  // helpers fenced their stores before counting; order them before our release
+                __syncwarp();
+                return true;
+            }
+        }
+        warp_merge(buf(a, depth + 1u), buf(a, depth), l, m, m, r, l, lane, T);
+        return true;
+    }
+
+    // claim and merge chunks of the block's open board until none is left (all 32 lanes)
+    __device__ __noinline__ static void help_chunks(const Args& a, MergeSlotHolder* H, uint32_t lane, WarpTiles* T) {
+        volatile MergeSlotHolder::Board& B = H->board;
+        while (true) {
+            uint32_t c = 0;
+            if (lane == 0) c = atomicAdd(&H->board.next, 1u);
+            c = __shfl_sync(0xffffffffu, c, 0);
+            __threadfence_block();
+            const uint32_t nch = B.nchunks;                // read after the claim (see assist)
+            if (c >= nch) break;
+            const uint32_t l = B.l, m = B.m, r = B.r, depth = B.depth;
+            const int32_t* src = buf(a, depth + 1u);
+            const uint32_t n = r - l, o0 = c * kChunk, o1 = min(n, o0 + kChunk);
+            const uint32_t i0 = warp_split(src, l, m, r, o0, lane), i1 = warp_split(src, l, m, r, o1, lane);
+            warp_merge(src, buf(a, depth), l + i0, l + i1, m + (o0 - i0), m + (o1 - i1), l + o0, lane, T);
+            if (lane == 0) atomicAdd(&H->board.done, 1u);  // warp_merge fenced the chunk's stores
+        }
+    }
+
+    // scheduler hook, top of every cycle (all 32 lanes): join an open board of this block
+    __device__ __forceinline__ static void help(const Args& a, uint32_t lane, MergeSlotHolder* H) {
+        if (reinterpret_cast<volatile uint32_t&>(H->board.state) == 2u)
+            help_chunks(a, H, lane, H->tiles(threadIdx.x >> 5));
+    }
     using BlockExtra = MergeSlotHolder;
     __device__ __forceinline__ static void block_init(BlockExtra* H) {
         MergeSlot* S = H->slot();
@@ -562,6 +776,10 @@ struct MergesortTable {
             S->par[k] = 0;
         }
         H->busy = 0;
+        H->board.state = 0;
+        H->board.next = 0x80000000u;
+        H->board.nchunks = 0;
+        H->board.done = 0;
         tma::fence_smem();
     }
 
@@ -638,6 +856,11 @@ struct MergesortTable {
                     return;
                 }
             case 1: {
+                if (a.mode == 1u && r - l >= kAssistMin) {  // merge(l, m, r) by the whole warp
+                    o.request_assist(l, r, depth, 0u);
+                    o.finish_void();
+                    return;
+                }
                 const uint32_t m = l + (r - l) / 2u;
                 if (!merge(a, buf(a, depth + 1u), buf(a, depth), l, m, r, S)) { o.bad_state(); return; }
                 o.finish_void();
@@ -656,8 +879,14 @@ static int validate_ms(const gtap_task_table* t, uint32_t fn, const uint32_t* d)
 
 }  // namespace gtap
 
-extern "C" const gtap_task_table* gtap_table_mergesort(int32_t* keys, int32_t* scratch, uint64_t n, int32_t cutoff) {
+extern "C" const gtap_task_table* gtap_table_mergesort_ex(int32_t* keys, int32_t* scratch, uint64_t n, int32_t cutoff,
+                                                         uint32_t merge_mode) {
     if (((!keys || !scratch) && n > 0) || cutoff < 1 || cutoff > gtap::kMsMaxCutoff || n >= (1ull << 31)) return nullptr;
-    gtap::MergesortTable::Args a{keys, scratch, (uint32_t)cutoff, (uint32_t)n};
+    if (merge_mode > 1u) return nullptr;
+    gtap::MergesortTable::Args a{keys, scratch, (uint32_t)cutoff, (uint32_t)n, merge_mode, 0u};
     return gtap::make_table<gtap::MergesortTable>("mergesort", a, &gtap::validate_ms);
+}
+
+extern "C" const gtap_task_table* gtap_table_mergesort(int32_t* keys, int32_t* scratch, uint64_t n, int32_t cutoff) {
+    return gtap_table_mergesort_ex(keys, scratch, n, cutoff, 1u);
 }

@@ -51,7 +51,7 @@ class Stats(ctypes.Structure):
         ("stolen_tasks", ctypes.c_uint64), ("pushes", ctypes.c_uint64), ("cycles", ctypes.c_uint64),
         ("idle_cycles", ctypes.c_uint64), ("remote_frees", ctypes.c_uint64), ("max_pool_used", ctypes.c_uint64),
         ("error_word", ctypes.c_uint32), ("workers", ctypes.c_uint32), ("device_ms", ctypes.c_float),
-        ("grid_size", ctypes.c_uint32), ("block_size", ctypes.c_uint32), ("reserved", ctypes.c_uint32 * 2),
+        ("grid_size", ctypes.c_uint32), ("block_size", ctypes.c_uint32), ("assists", ctypes.c_uint32), ("reserved", ctypes.c_uint32),
     ]
 
     def as_dict(self) -> dict:
@@ -62,7 +62,7 @@ class Stats(ctypes.Structure):
 EXPORTS = [
     "gtap_abi_version", "gtap_status_str", "gtap_config_default", "gtap_workspace_bytes", "gtap_init",
     "gtap_spawn_root", "gtap_reset", "gtap_run", "gtap_sync", "gtap_root_result", "gtap_finalize",
-    "gtap_geometry", "gtap_table_destroy", "gtap_table_fib", "gtap_table_fib_cutoff", "gtap_table_nqueens", "gtap_table_tree", "gtap_table_mergesort", "gtap_table_cilksort",
+    "gtap_geometry", "gtap_table_destroy", "gtap_table_fib", "gtap_table_fib_cutoff", "gtap_table_nqueens", "gtap_table_tree", "gtap_table_mergesort", "gtap_table_mergesort_ex", "gtap_table_cilksort",
     "gtap_table_spmv",
     "gtap_table_bfs", "gtap_bfs_init_depth", "gtap_ubench_atomics",
 ]
@@ -107,6 +107,8 @@ def lib():
     L.gtap_table_tree.restype = vp
     L.gtap_table_mergesort.argtypes = [vp, vp, u64, i32]
     L.gtap_table_mergesort.restype = vp
+    L.gtap_table_mergesort_ex.argtypes = [vp, vp, u64, i32, ctypes.c_uint32]
+    L.gtap_table_mergesort_ex.restype = vp
     L.gtap_table_cilksort.argtypes = [vp, vp, u64, i32, i32]
     L.gtap_table_cilksort.restype = vp
     L.gtap_table_spmv.argtypes = [vp, vp, vp, vp, vp, u32, u32, u32]
@@ -189,11 +191,13 @@ class Table:
         return Table(lib().gtap_table_nqueens(n, cutoff, count.data_ptr()), "nqueens", GTAP_WORKER_THREAD, (count,))
 
     @staticmethod
-    def mergesort(keys, scratch, cutoff: int = 128) -> "Table":
+    def mergesort(keys, scratch, cutoff: int = 128, merge_mode: int = 1) -> "Table":
+        """merge_mode: GTAP_MERGE_WARP (1, default) or GTAP_MERGE_THREAD (0, the paper's one-lane merge)."""
         _dev_i32(keys, "keys"); _dev_i32(scratch, "scratch")
         if scratch.numel() < keys.numel():
             raise ValueError("scratch must hold n keys")
-        return Table(lib().gtap_table_mergesort(keys.data_ptr(), scratch.data_ptr(), keys.numel(), cutoff),
+        return Table(lib().gtap_table_mergesort_ex(keys.data_ptr(), scratch.data_ptr(), keys.numel(), cutoff,
+                                                   merge_mode),
                      "mergesort", GTAP_WORKER_THREAD, (keys, scratch))
 
     @staticmethod
@@ -243,6 +247,7 @@ class RunStats:
     device_ms: float
     grid_size: int
     block_size: int
+    assists: int = 0
 
 
 class Runtime:

@@ -3,7 +3,9 @@
 PAPER.md P:59-74. Ragged sizes around the cutoff and the
 32-lane tile, every cutoff the API allows at its edges, adversarial inputs,
 forests, and BASELINE configs[1] (2^24 random int32) at the bench's launch
-configuration.
+configuration. Every test runs in both merge modes: GTAP_MERGE_THREAD (the
+paper's one-lane merge, TMA-staged for long runs) and GTAP_MERGE_WARP (heavy
+merges run by the task's whole warp).
 """
 import numpy as np
 import pytest
@@ -21,6 +23,11 @@ def g(cuda_device):
     return g
 
 
+@pytest.fixture(scope="module", params=[0, 1], ids=["thread_merge", "warp_merge"])
+def mode(request):
+    return request.param
+
+
 @pytest.fixture(scope="module")
 def rt(g):
     r = g.Runtime(g.GTAP_WORKER_THREAD, 0, grid_size=148 * 2, block_size=128, max_tasks_per_worker=1024,
@@ -29,10 +36,10 @@ def rt(g):
     r.close()
 
 
-def run_sort(g, rt, keys_np, cutoff=128):
+def run_sort(g, rt, keys_np, cutoff=128, mode=1):
     import torch
     d = torch.from_numpy(keys_np).cuda()
-    st = g.mergesort_(d, cutoff=cutoff, rt=rt)
+    st = g.mergesort_(d, cutoff=cutoff, merge_mode=mode, rt=rt)
     return d.cpu().numpy(), st
 
 
@@ -40,42 +47,56 @@ def run_sort(g, rt, keys_np, cutoff=128):
 # other sizes exercise the register-window merge
 @pytest.mark.parametrize("n", [0, 1, 2, 31, 127, 128, 129, 255, 256, 1000, 4097, (1 << 16) + 7, 1 << 20,
                                100004, 3 * (1 << 18) + 12, 40000])
-def test_sizes(g, rt, n):
+def test_sizes(g, rt, mode, n):
     keys = synth.keys_int32(n, seed=n).numpy()
-    out, st = run_sort(g, rt, keys)
+    out, st = run_sort(g, rt, keys, 128, mode)
     ref, tasks, inv = oracle.mergesort(keys, 128)
     assert np.array_equal(out, ref)
     assert (st.tasks, st.invocations) == (tasks, inv)
+    if mode == 0 or n < 8192:
+        assert st.assists == 0
+    else:  # every merge of >= 8192 keys ran as a warp assist
+        assert st.assists == sum(1 for r in _merge_sizes(n, 128) if r >= 8192)
+
+
+def _merge_sizes(n, cutoff):
+    out, stack = [], [n]
+    while stack:
+        k = stack.pop()
+        if k > cutoff:
+            out.append(k)
+            stack += [k // 2, k - k // 2]
+    return out
 
 
 @pytest.mark.parametrize("cutoff", [1, 2, 3, 64, 128, 255, 256])
-def test_cutoffs(g, rt, cutoff):
+def test_cutoffs(g, rt, mode, cutoff):
     keys = synth.keys_int32(20011, seed=cutoff).numpy()
-    out, st = run_sort(g, rt, keys, cutoff)
+    out, st = run_sort(g, rt, keys, cutoff, mode)
     ref, tasks, inv = oracle.mergesort(keys, cutoff)
     assert np.array_equal(out, ref)
     assert (st.tasks, st.invocations) == (tasks, inv)
 
 
 @pytest.mark.parametrize("kind", ["sorted", "reverse", "equal", "two", "extremes"])
-def test_adversarial(g, rt, kind):
-    n = 100003
+@pytest.mark.parametrize("n", [100003, 300007])   # 300007: block-assisted top merge (>= 2^17), chunk borders on ties
+def test_adversarial(g, rt, mode, kind, n):
     rng = np.random.default_rng(7)
     a = {"sorted": np.arange(n), "reverse": np.arange(n, 0, -1), "equal": np.full(n, 3),
          "two": rng.integers(0, 2, n),
          "extremes": rng.choice(np.array([-2**31, 2**31 - 1, 0, -1]), n)}[kind].astype(np.int32)
-    out, _ = run_sort(g, rt, a)
+    out, _ = run_sort(g, rt, a, 128, mode)
     assert np.array_equal(out, oracle.mergesort(a, 128)[0])
 
 
-def test_forest(g):
+def test_forest(g, mode):
     import torch
     seg = 1 << 14
     k = 37  # total length 37 * 2^14 + 5: register-window merges
     keys = synth.keys_int32(seg * k + 5, seed=3).numpy()
     segments = [(i * seg, (i + 1) * seg) for i in range(k)] + [(seg * k, seg * k + 5)]
     d = torch.from_numpy(keys).cuda()
-    st = g.mergesort_forest_(d, segments, grid_size=148, block_size=128, max_tasks_per_worker=1024,
+    st = g.mergesort_forest_(d, segments, merge_mode=mode, grid_size=148, block_size=128, max_tasks_per_worker=1024,
                              watchdog_ns=WD)
     out = d.cpu().numpy()
     tasks = 0
@@ -86,7 +107,7 @@ def test_forest(g):
     assert st.tasks == tasks
 
 
-def test_full_size_config1(g):
+def test_full_size_config1(g, mode):
     """BASELINE configs[1]: 2^24 random int32 keys, cutoff 128, the bench's launch configuration."""
     import torch
 
@@ -95,13 +116,13 @@ def test_full_size_config1(g):
     keys = synth.keys_int32(n, seed=42)
     d = keys.cuda()
     with g.Runtime(g.GTAP_WORKER_THREAD, 0, watchdog_ns=60_000_000_000, **bench.MS_CFG) as r:
-        st = g.mergesort_(d, cutoff=128, rt=r)
+        st = g.mergesort_(d, cutoff=128, merge_mode=mode, rt=r)
     ref, tasks, inv = oracle.mergesort(keys.numpy(), 128)
     assert np.array_equal(d.cpu().numpy(), ref)
     assert (st.tasks, st.invocations) == (tasks, inv) == (262143, 393214)
 
 
-def test_forest_tma_segments(g):
+def test_forest_tma_segments(g, mode):
     import torch
     # segment lengths multiple of 4 but not of the 512-key chunk: TMA merges with partial chunks,
     # neighbouring roots writing adjacent keys concurrently
@@ -110,7 +131,7 @@ def test_forest_tma_segments(g):
     keys = synth.keys_int32(int(bounds[-1]), seed=9).numpy()
     d = torch.from_numpy(keys).cuda()
     segs = [(int(bounds[i]), int(bounds[i + 1])) for i in range(len(lens))]
-    g.mergesort_forest_(d, segs, grid_size=148, block_size=128, max_tasks_per_worker=1024, watchdog_ns=WD)
+    g.mergesort_forest_(d, segs, merge_mode=mode, grid_size=148, block_size=128, max_tasks_per_worker=1024, watchdog_ns=WD)
     out = d.cpu().numpy()
     for l, r in segs:
         assert np.array_equal(out[l:r], np.sort(keys[l:r]))

@@ -36,7 +36,9 @@ if ROOT not in sys.path:
 # ---- launch configurations (shared with the full-size parity tests) ----------
 MS_N = 1 << 24
 MS_CUTOFF = 128
-MS_CFG = dict(grid_size=0, block_size=128, max_tasks_per_worker=1024, idle_backoff_ns=32768)
+MS_CFG = dict(grid_size=0, block_size=128, max_tasks_per_worker=1024, idle_backoff_ns=1024)
+MS_MERGE_MODE = 1        # GTAP_MERGE_WARP: leaf/merge bodies run by the task's warp (+ block / GPU-wide assist)
+MS0_CFG = dict(grid_size=0, block_size=128, max_tasks_per_worker=1024, idle_backoff_ns=32768)  # one-lane merge
 FIB_N = 40
 FIB_CFG = dict(grid_size=0, block_size=128, max_tasks_per_worker=4096)
 SPMV_ROWS = 1 << 22
@@ -159,7 +161,7 @@ def bench_mergesort(args, ws, rank, dev):
     scratch = torch.empty_like(pristine)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
     rt = g.Runtime(g.GTAP_WORKER_THREAD, dev.index, **MS_CFG)
-    table = g.Table.mergesort(keys, scratch, MS_CUTOFF)
+    table = g.Table.mergesort(keys, scratch, MS_CUTOFF, MS_MERGE_MODE)
     stream = torch.cuda.current_stream()
 
     def step(timed_events=None):
@@ -205,7 +207,7 @@ def bench_mergesort(args, ws, rank, dev):
         a.record(stream)
         keys.copy_(host_in, non_blocking=True)
         rt.reset(stream)
-        g.mergesort_(keys, scratch, MS_CUTOFF, rt=rt, stream=stream)
+        g.mergesort_(keys, scratch, MS_CUTOFF, merge_mode=MS_MERGE_MODE, rt=rt, stream=stream)
         host_out.copy_(keys, non_blocking=True)
         b.record(stream)
         torch.cuda.synchronize()
@@ -215,7 +217,6 @@ def bench_mergesort(args, ws, rank, dev):
     algo_bytes = 8.0 * n * (1 + _ms_levels(n, MS_CUTOFF))  # read+write per key per pass
     pk, src = peaks()
     achieved = algo_bytes / (ms * 1e-3) / 1e9
-    span_steps = 2 * n  # sequential merge steps on the critical path (top merge n + next n/2 + ...)
     res = dict(
         value=ws * n / (ms_max * 1e-3) / 1e6, ms_per_step=ms_max, wall_ms_per_step=wall * 1e3 / args.steps,
         event_ms_per_step=statistics.mean(ev_ms),
@@ -224,11 +225,11 @@ def bench_mergesort(args, ws, rank, dev):
         roofline=dict(bound="hbm", achieved=achieved, peak=pk["hbm_gbs"], unit="GB/s",
                       frac=achieved / pk["hbm_gbs"], traffic=profile_traffic("mergesort"),
                       peak_source=src, algorithmic_bytes_per_launch=algo_bytes,
-                      note="span-bound by design: the top merge is one thread (P:593); "
-                           f"critical path ~{span_steps} sequential merge steps, "
-                           f"{ms * 1e6 / span_steps:.2f} ns per step"),
+                      algorithmic_bytes_per_key=8.0 * (1 + _ms_levels(n, MS_CUTOFF)),
+                      note="8 B/key (read + write) for the leaf pass and each of the merge levels; the "
+                           "persistent scheduler kernel is the only kernel of the step"),
         stats=dict(tasks=st.tasks, invocations=st.invocations, steals_ok=st.steals_ok, workers=st.workers,
-                   grid=st.grid_size, block=st.block_size),
+                   grid=st.grid_size, block=st.block_size, assists=st.assists),
         correct=ok, clocks=clk.summary(), gpu_launches=args.steps,
     )
     rt.close()
@@ -242,6 +243,30 @@ def _ms_levels(n, c):
         n = (n + 1) // 2
         lv += 1
     return lv
+
+
+def bench_mergesort_thread_merge(dev, reps=2):
+    """The paper's one-lane merge (GTAP_MERGE_THREAD): same task graph, every leaf sort and
+    merge body on its task's own lane (long merges TMA-staged); span-bound by the top merge."""
+    import torch
+
+    import synth
+    import paper_2604_05982_b200 as g
+    keys0 = synth.keys_int32(MS_N, seed=42, device=dev)
+    keys = torch.empty_like(keys0)
+    scratch = torch.empty_like(keys0)
+    ms = []
+    with g.Runtime(g.GTAP_WORKER_THREAD, dev.index, **MS0_CFG) as rt:
+        for i in range(reps + 1):
+            keys.copy_(keys0)
+            st = g.mergesort_(keys, scratch, MS_CUTOFF, merge_mode=0, rt=rt)
+            if i:
+                ms.append(st.device_ms)
+    t = statistics.median(ms)
+    assert bool(torch.all(keys[1:] >= keys[:-1]).item())
+    return dict(workload="mergesort 2^24 cutoff 128, merge_mode=thread (paper's one-lane merge, P:593)",
+                metric="Mkeys/s", value=MS_N / (t * 1e-3) / 1e6, ms=t, launch=MS0_CFG,
+                span_note=f"critical path ~{2 * MS_N} sequential merge steps, {t * 1e6 / (2 * MS_N):.2f} ns/step")
 
 
 def bench_fib(dev, reps=3):
@@ -468,6 +493,7 @@ def run_ours(args):
             secondary.append(dict(workload="L2 atomic probes", metric="ops/s", value=atoms))
             secondary.append(bench_epaq(dev))
             secondary.append(bench_nqueens(dev))
+            secondary.append(bench_mergesort_thread_merge(dev))
             secondary.append(bench_cilksort(dev))
             secondary.append(bench_tree(dev))
         except Exception as e:  # secondary results must not kill the main line
@@ -496,6 +522,9 @@ def run_ours(args):
             "config": {"workload": "mergesort 2^24 random int32 keys, thread-level fork-join, cutoff 128 "
                                    "(BASELINE configs[1])",
                        "keys_per_gpu": MS_N, "cutoff": MS_CUTOFF, "launch": MS_CFG,
+                       "merge_mode": "warp (GTAP_MERGE_WARP: thread-level tasks, leaf-sort and merge bodies run "
+                                     "by the task's warp, long merges shared by idle warps; same task graph -- "
+                                     "the paper's one-lane merge is the secondary 'merge_mode=thread' line)",
                        "grid": res["stats"]["grid"], "block": res["stats"]["block"],
                        "workers": res["stats"]["workers"], "l2": "flushed between steps (256 MiB write)",
                        "parallelism": f"replicas x{ws} (independent roots per GPU)",

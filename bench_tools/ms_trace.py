@@ -1,29 +1,51 @@
-"""Per-merge trace of one 2^24 mergesort (needs libgtap_gtap_ms_trace.so)."""
-import sys, os, ctypes, json
+"""Timeline of one 2^24 mergesort (merge_mode 1 by default) from the GTAP_MS_TRACE build.
+
+usage: python bench_tools/ms_trace.py [merge_mode] [idle_backoff_ns]
+Per (kind, size): count, first start / last end (ms from the first record), mean duration.
+"""
+import ctypes
+import os
+import sys
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-os.environ["GTAP_LIB"] = os.path.join(ROOT, "paper_2604_05982_b200", "libgtap_gtap_ms_trace.so")
+os.environ.setdefault("GTAP_LIB", os.path.join(ROOT, "paper_2604_05982_b200", "libgtap_gtap_ms_trace.so"))
 sys.path.insert(0, ROOT)
-import numpy as np, torch, synth, bench
-import paper_2604_05982_b200 as g
-from paper_2604_05982_b200 import gtap
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_2604_05982_b200 as g  # noqa: E402
+import synth  # noqa: E402
+from paper_2604_05982_b200 import gtap  # noqa: E402
+
+mode = int(sys.argv[1]) if len(sys.argv) > 1 else 1
+backoff = int(sys.argv[2]) if len(sys.argv) > 2 else bench.MS_CFG["idle_backoff_ns"]
+KIND = {0: "lane merge", 1: "TMA merge", 2: "leaf sort", 3: "warp assist", 4: "block assist", 5: "GPU assist",
+        6: "GPU chunk", 7: "block chunk"}
 n = 1 << 24
-keys = synth.keys_int32(n, seed=42, device="cuda"); scratch = torch.empty_like(keys)
+keys = synth.keys_int32(n, seed=42, device="cuda")
+scratch = torch.empty_like(keys)
 L = gtap.lib()
-buf = np.zeros((65536, 4), np.uint64); cnt = ctypes.c_uint32()
-with g.Runtime(g.GTAP_WORKER_THREAD, 0, **bench.MS_CFG) as rt:
-    st = g.mergesort_(keys.clone(), scratch, 128, rt=rt)
-    L.gtap_ms_trace_read(buf.ctypes.data_as(ctypes.c_void_p), ctypes.byref(cnt))
-    k2 = keys.clone()
-    st = g.mergesort_(k2, scratch, 128, rt=rt)
-    L.gtap_ms_trace_read(buf.ctypes.data_as(ctypes.c_void_p), ctypes.byref(cnt))
-m = int(cnt.value)
-t0, t1, sz, sm = buf[:m, 0].astype(np.int64), buf[:m, 1].astype(np.int64), (buf[:m, 2] >> np.uint64(32)).astype(np.int64), buf[:m, 3]
+cap = 1 << 20
+buf = np.zeros((cap, 4), np.uint64)
+cnt = ctypes.c_uint32()
+with g.Runtime(g.GTAP_WORKER_THREAD, 0, **dict(bench.MS_CFG, idle_backoff_ns=backoff)) as rt:
+    for _ in range(2):
+        k2 = keys.clone()
+        L.gtap_ms_trace_read(buf.ctypes.data_as(ctypes.c_void_p), ctypes.byref(cnt))
+        st = g.mergesort_(k2, scratch, 128, merge_mode=mode, rt=rt)
+        L.gtap_ms_trace_read(buf.ctypes.data_as(ctypes.c_void_p), ctypes.byref(cnt))
+m = min(int(cnt.value), cap)
+t0, t1 = buf[:m, 0].astype(np.int64), buf[:m, 1].astype(np.int64)
+sz = (buf[:m, 2] >> np.uint64(32)).astype(np.int64)
+kind = (buf[:m, 3] & np.uint64(255)).astype(np.int64)
 base = t0.min()
-print("kernel ms", st.device_ms, "merges traced", m)
-for size in sorted(set(sz.tolist()), reverse=True)[:14]:
-    sel = sz == size
-    used = (sm[sel] & np.uint64(1)).astype(int)
-    d = (t1[sel] - t0[sel]) / 1e6
-    print(f"size={size:9d} count={sel.sum():5d} tma={used.sum():5d} dur_ms min={d.min():8.3f} max={d.max():8.3f} "
-          f"ns/key={d.max()*1e6/size:6.2f} start_ms={(t0[sel].min()-base)/1e6:8.3f} end_ms={(t1[sel].max()-base)/1e6:8.3f} "
-          f"distinct_sm={len(set((sm[sel] >> np.uint64(8)).tolist()))}")
+print(f"mode={mode} backoff={backoff} kernel_ms={st.device_ms:.3f} records={m} span_ms={(t1.max() - base) / 1e6:.3f}")
+for k in sorted(set(kind.tolist())):
+    for size in sorted(set(sz[kind == k].tolist()), reverse=True):
+        sel = (kind == k) & (sz == size)
+        if sel.sum() < 1:
+            continue
+        d = (t1[sel] - t0[sel]) / 1e3
+        print(f"{KIND[k]:12s} size={size:9d} n={sel.sum():6d} start={(t0[sel].min() - base) / 1e6:7.3f} "
+              f"end={(t1[sel].max() - base) / 1e6:7.3f} ms  dur_us mean={d.mean():8.1f} max={d.max():8.1f}")

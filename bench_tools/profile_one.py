@@ -16,7 +16,7 @@ if wl == "ms":
     with g.Runtime(g.GTAP_WORKER_THREAD, 0, **bench.MS_CFG) as rt:
         for i in range(reps):
             keys.copy_(pristine)
-            st = g.mergesort_(keys, scratch, 128, rt=rt)
+            st = g.mergesort_(keys, scratch, 128, merge_mode=bench.MS_MERGE_MODE, rt=rt)
             print("ms", n, st.device_ms, flush=True)
 elif wl == "fib":
     n = size or 30

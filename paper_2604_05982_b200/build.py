@@ -26,32 +26,33 @@ SOURCES = ["runtime.cu", "table_fib.cu", "table_mergesort.cu", "table_spmv.cu", 
            "table_cilksort.cu", "table_tree.cu", "ubench.cu"]
 
 
-def _digest() -> str:
+def _digest(lib: str, extra) -> str:
     h = hashlib.sha256()
     for d in (CSRC, INCLUDE):
         for f in sorted(os.listdir(d)):
             if f.endswith((".cu", ".cuh", ".h")):
                 with open(os.path.join(d, f), "rb") as fh:
                     h.update(f.encode() + fh.read())
-    h.update(" ".join(ARCH + FLAGS).encode() + LIB.encode())
+    h.update(" ".join(ARCH + FLAGS + list(extra)).encode() + lib.encode())
     return h.hexdigest()
 
 
 def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False, defines=(), out=None) -> str:
     """Compile every .cu in SOURCES and link libgtap.so (out/defines: diagnostic variants only)."""
-    global LIB, BUILD
+    lib, bdir = LIB, BUILD
     if defines or out:
-        LIB = out or LIB.replace(".so", "_" + "_".join(d.lower() for d in defines) + ".so")
-        BUILD = BUILD + "_" + "_".join(d.lower() for d in defines)
-    os.makedirs(BUILD, exist_ok=True)
-    stamp = os.path.join(BUILD, "stamp")
-    dig = _digest()
-    if not force and os.path.exists(LIB) and os.path.exists(stamp) and open(stamp).read() == dig:
-        return LIB
+        tag = "_".join(d.lower().replace("=", "") for d in defines)
+        lib = out or LIB.replace(".so", "_" + tag + ".so")
+        bdir = BUILD + "_" + tag
+    os.makedirs(bdir, exist_ok=True)
+    stamp = os.path.join(bdir, "stamp")
     extra = (["-Xptxas", "-v"] if ptxas_v else []) + [f"-D{d}" for d in defines]
+    dig = _digest(lib, [f"-D{d}" for d in defines])
+    if not force and os.path.exists(lib) and os.path.exists(stamp) and open(stamp).read() == dig:
+        return lib
 
     def compile_one(src):
-        obj = os.path.join(BUILD, src.replace(".cu", ".o"))
+        obj = os.path.join(bdir, src.replace(".cu", ".o"))
         cmd = [NVCC, *ARCH, *FLAGS, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
@@ -63,15 +64,15 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False, def
     if verbose or ptxas_v:
         for _, err in results:
             sys.stderr.write(err)
-    tmp = LIB + f".{os.getpid()}.tmp"
+    tmp = lib + f".{os.getpid()}.tmp"
     cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *[o for o, _ in results], "-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib)
     with open(stamp, "w") as f:
         f.write(dig)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

@@ -304,6 +304,7 @@ gtap_status gtap_run(gtap_runtime* rt, void* stream) {
     p.roots = reinterpret_cast<const RootSpec*>(rt->ws + rt->L.roots);
     p.root_results = reinterpret_cast<long long*>(rt->ws + rt->L.results);
 
+    if (rt->table->prepare && rt->table->prepare(rt->table, s) != cudaSuccess) return GTAP_E_CUDA;
     if (cudaEventRecord(rt->ev0, s) != cudaSuccess) return GTAP_E_CUDA;
     const cudaError_t le = rt->table->launch(rt->table, p, grid, block, s);
     if (le != cudaSuccess) return GTAP_E_CUDA;
@@ -381,7 +382,10 @@ gtap_status gtap_finalize(gtap_runtime* rt) {
     return GTAP_OK;
 }
 
-void gtap_table_destroy(const gtap_task_table* t) { delete const_cast<gtap_task_table*>(t); }
+void gtap_table_destroy(const gtap_task_table* t) {
+    if (t && t->dev_scratch) cudaFree(t->dev_scratch);
+    delete const_cast<gtap_task_table*>(t);
+}
 
 
 }  // extern "C"

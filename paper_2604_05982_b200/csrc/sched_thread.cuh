@@ -351,6 +351,9 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
             d = __shfl_sync(0xffffffffu, d, 0);
             if (d) break;
             if (p.watchdog_ns && lane == 0 && globaltimer() - t0 > p.watchdog_ns) raise_error(p.ctl, GTAP_E_TIMEOUT);
+            if constexpr (assist_of<T>::value) {
+                if (T::help_idle(args, lane, bx)) { backoff = 32; continue; }  // helped an open assist
+            }
             nanosleep(backoff);
             backoff = min(backoff * 2u, p.idle_backoff);
             continue;
@@ -384,9 +387,10 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
         if constexpr (assist_of<T>::value) {
             // (2b) warp assist: lanes whose body deferred a heavy leaf routine get the whole warp,
             // one request at a time (a B200 choice; the task graph and
-            // the result are unchanged). T::assist fences its writes and syncs the warp, so the
-            // requesting lane's join release below covers every lane's stores.
+            // the result are unchanged). One fence + warp sync after the requests, so the
+            // requesting lanes' join releases below cover every lane's stores.
             uint32_t req = __ballot_sync(0xffffffffu, my != kNone && o.assist != 0u && o.err == 0u);
+            const bool any_assist = req != 0u;
             while (req) {
                 const uint32_t src = (uint32_t)__ffs(req) - 1u;
                 req &= req - 1u;
@@ -397,6 +401,10 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
                 const uint32_t okm = __ballot_sync(0xffffffffu, aok);
                 if (lane == src && okm != 0xffffffffu) o.err = GTAP_E_BAD_STATE;
                 if (lane == 0) ++st_assist;
+            }
+            if (any_assist) {
+                __threadfence();
+                __syncwarp();
             }
         }
         __syncwarp();

@@ -22,6 +22,10 @@ struct gtap_task_table {
                           cudaStream_t);
     cudaError_t (*occupancy)(const gtap_task_table*, uint32_t block, int* blocks_per_sm, size_t* smem);
     int (*validate_root)(const gtap_task_table*, uint32_t fn, const uint32_t* d);
+    // optional: device memory owned by the table (freed by gtap_table_destroy) and a per-run
+    // reset enqueued by gtap_run before the launch
+    void* dev_scratch = nullptr;
+    cudaError_t (*prepare)(const gtap_task_table*, cudaStream_t) = nullptr;
     alignas(16) unsigned char args[128];
 };
 

@@ -167,15 +167,35 @@ constexpr uint32_t kRingMaskB = kRing * 4u - 1u;
 constexpr uint32_t kTmaMin = 8192;           // merges at least this long take the TMA path
 constexpr uint32_t kNoChunk = 0x80000000u;
 #ifdef GTAP_MS_TRACE
-__device__ ulonglong4 gtap_ms_trace[65536];
+// diagnostic build only: one record per merge / leaf / assist / chunk:
+// {t0, t1, size << 32 | l, smid << 8 | kind}; kinds: 0 lane merge, 1 TMA merge, 2 leaf sort,
+// 3 warp assist, 4 block assist (requester), 5 GPU-wide assist (requester), 6 GPU-wide chunk, 7 block chunk
+constexpr uint32_t kMsTraceCap = 1u << 20;
+__device__ ulonglong4 gtap_ms_trace[kMsTraceCap];
 __device__ uint32_t gtap_ms_trace_n;
 extern "C" int gtap_ms_trace_read(void* host, uint32_t* n) {
     cudaMemcpyFromSymbol(n, gtap_ms_trace_n, 4);
-    cudaMemcpyFromSymbol(host, gtap_ms_trace, sizeof(ulonglong4) * (*n < 65536u ? *n : 65536u));
+    cudaMemcpyFromSymbol(host, gtap_ms_trace, sizeof(ulonglong4) * (*n < kMsTraceCap ? *n : kMsTraceCap));
     const uint32_t z = 0;
     cudaMemcpyToSymbol(gtap_ms_trace_n, &z, 4);
     return 0;
 }
+__device__ __forceinline__ void ms_trace(unsigned long long t0, uint32_t size, uint32_t l, uint32_t kind) {
+    const uint32_t i = atomicAdd(&gtap_ms_trace_n, 1u);
+    if (i < kMsTraceCap) {
+        unsigned smid;
+        asm("mov.u32 %0, %%smid;" : "=r"(smid));
+        gtap_ms_trace[i] = make_ulonglong4(t0, dev::globaltimer(), ((unsigned long long)size << 32) | l,
+                                           ((unsigned long long)smid << 8) | kind);
+    }
+}
+#define MS_T0 const unsigned long long ms_t0 = dev::globaltimer()
+#define MS_TRACE(size, l, kind) ms_trace(ms_t0, (size), (l), (kind))
+#define MS_TRACE_LANE0(size, l, kind) do { if (lane == 0) ms_trace(ms_t0, (size), (l), (kind)); } while (0)
+#else
+#define MS_T0 do {} while (0)
+#define MS_TRACE(size, l, kind) do {} while (0)
+#define MS_TRACE_LANE0(size, l, kind) do {} while (0)
 #endif
 
 struct MergeSlot {                           // placed 2 KB-aligned inside the block's dynamic smem
@@ -657,28 +677,182 @@ __device__ __noinline__ void warp_merge(const int32_t* __restrict__ src, int32_t
     __syncwarp();
 }
 
-// all 32 lanes: stable merge-path split (A keys among the first t outputs of merge(src[l, m), src[m, r)))
-// over global memory, 32 probes per step (a ~33-way search: ~5 dependent round trips for 2^23 keys)
-__device__ __noinline__ uint32_t warp_split(const int32_t* src, uint32_t l, uint32_t m, uint32_t r, uint32_t t,
-                                            uint32_t lane) {
-    uint32_t lo = t > (r - m) ? t - (r - m) : 0u, hi = min(t, m - l);
-    while (hi - lo > 32u) {
-        const uint32_t w = hi - lo;
-        const uint32_t q = lo + (uint32_t)(((unsigned long long)(lane + 1u) * w) / 33u);
-        const bool pr = __ldcg(src + l + q) <= __ldcg(src + m + (t - q - 1u));
-        const uint32_t cnt = (uint32_t)__popc(__ballot_sync(0xffffffffu, pr));  // trues form a prefix
-        const uint32_t qlo = __shfl_sync(0xffffffffu, q, (cnt + 31u) & 31u);
-        const uint32_t qhi = __shfl_sync(0xffffffffu, q, cnt & 31u);
-        if (cnt > 0u) lo = qlo + 1u;
-        if (cnt < 32u) hi = qhi;
+// all 32 lanes: sort the x[k] (element k * 32 + lane) ascending by a bitonic network (shuffles
+// for partners in other lanes, register compare-exchange for partners in the same lane)
+template <int K>
+__device__ __forceinline__ void warp_bitonic(int32_t (&x)[K], uint32_t lane) {
+    constexpr int N = 32 * K;
+#pragma unroll
+    for (int size = 2; size <= N; size <<= 1) {
+#pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            if (stride >= 32) {
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    const int kk = k ^ (stride >> 5);
+                    if (kk > k) {
+                        const bool up = (((uint32_t)k * 32u + lane) & (uint32_t)size) == 0u;
+                        const int32_t a = x[k], b = x[kk];
+                        const bool sw = up ? (a > b) : (a < b);
+                        x[k] = sw ? b : a;
+                        x[kk] = sw ? a : b;
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    const int32_t p = __shfl_xor_sync(0xffffffffu, x[k], stride);
+                    const bool up = (((uint32_t)k * 32u + lane) & (uint32_t)size) == 0u;
+                    const bool lower = (lane & (uint32_t)stride) == 0u;
+                    x[k] = (lower == up) ? min(x[k], p) : max(x[k], p);
+                }
+            }
+        }
     }
-    const uint32_t q = lo + lane;
-    const bool pr = q < hi && __ldcg(src + l + q) <= __ldcg(src + m + (t - q - 1u));
-    return lo + (uint32_t)__popc(__ballot_sync(0xffffffffu, pr));
+}
+
+// all 32 lanes: src[l, r) sorted into dst[l, r) (r - l <= 32 K), padded with INT32_MAX
+template <int K>
+__device__ __noinline__ void warp_leaf_sort_k(const int32_t* __restrict__ src, int32_t* __restrict__ dst, uint32_t l,
+                                              uint32_t r, uint32_t lane) {
+    const uint32_t n = r - l;
+    int32_t x[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const uint32_t i = (uint32_t)k * 32u + lane;
+        x[k] = i < n ? src[l + i] : INT_MAX;
+    }
+    warp_bitonic<K>(x, lane);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const uint32_t i = (uint32_t)k * 32u + lane;
+        if (i < n) dst[l + i] = x[k];
+    }
+}
+
+// all 32 lanes: merge of src[l, m) and src[m, r) (r - l <= 32 K) by one bitonic merge network:
+// A ascending, INT32_MAX padding, B reversed is a bitonic sequence of 32 K keys; log2(32 K) half-cleaner
+// stages sort it ascending and the first r - l keys are the merge (integer keys: equal keys are
+// indistinguishable, so the result is the stable merge's)
+template <int K>
+__device__ __noinline__ void warp_merge_bitonic_k(const int32_t* __restrict__ src, int32_t* __restrict__ dst,
+                                                  uint32_t l, uint32_t m, uint32_t r, uint32_t lane) {
+    constexpr uint32_t N = 32u * K;
+    const uint32_t na = m - l, nb = r - m;
+    int32_t x[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const uint32_t i = (uint32_t)k * 32u + lane;
+        x[k] = i < na ? src[l + i] : (i >= N - nb ? src[m + (N - 1u - i)] : INT_MAX);
+    }
+#pragma unroll
+    for (uint32_t stride = N >> 1; stride > 0; stride >>= 1) {
+        if (stride >= 32u) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const int kk = k ^ (int)(stride >> 5);
+                if (kk > k) {
+                    const int32_t a = x[k], b = x[kk];
+                    x[k] = min(a, b);
+                    x[kk] = max(a, b);
+                }
+            }
+        } else {
+            const bool lower = (lane & stride) == 0u;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const int32_t p = __shfl_xor_sync(0xffffffffu, x[k], stride);
+                x[k] = lower ? min(x[k], p) : max(x[k], p);
+            }
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const uint32_t i = (uint32_t)k * 32u + lane;
+        if (i < r - l) dst[l + i] = x[k];
+    }
+}
+
+constexpr uint32_t kBitonicMax = 1024;  // merges up to this many keys: one bitonic network
+
+__device__ __forceinline__ void warp_merge_small(const int32_t* src, int32_t* dst, uint32_t l, uint32_t m, uint32_t r,
+                                                 uint32_t lane) {
+    const uint32_t n = r - l;
+    if (n <= 32u) warp_merge_bitonic_k<1>(src, dst, l, m, r, lane);
+    else if (n <= 64u) warp_merge_bitonic_k<2>(src, dst, l, m, r, lane);
+    else if (n <= 128u) warp_merge_bitonic_k<4>(src, dst, l, m, r, lane);
+    else if (n <= 256u) warp_merge_bitonic_k<8>(src, dst, l, m, r, lane);
+    else if (n <= 512u) warp_merge_bitonic_k<16>(src, dst, l, m, r, lane);
+    else warp_merge_bitonic_k<32>(src, dst, l, m, r, lane);
+}
+
+__device__ __forceinline__ void warp_leaf_sort(const int32_t* src, int32_t* dst, uint32_t l, uint32_t r,
+                                               uint32_t lane) {
+    const uint32_t n = r - l;
+    if (n <= 32u) warp_leaf_sort_k<1>(src, dst, l, r, lane);
+    else if (n <= 64u) warp_leaf_sort_k<2>(src, dst, l, r, lane);
+    else if (n <= 128u) warp_leaf_sort_k<4>(src, dst, l, r, lane);
+    else warp_leaf_sort_k<8>(src, dst, l, r, lane);
+}
+
+// all 32 lanes: stable merge-path splits (A keys among the first t outputs of merge(src[l, m), src[m, r)))
+// over global memory, 32 probes per step (a ~33-way search: ~5 dependent round trips for 2^23 keys);
+// both splits of a chunk [t0, t1) in lockstep (one dependent round trip per step for the pair)
+__device__ __noinline__ uint2 warp_split2(const int32_t* src, uint32_t l, uint32_t m, uint32_t r, uint32_t t0,
+                                          uint32_t t1, uint32_t lane) {
+    uint32_t lo0 = t0 > (r - m) ? t0 - (r - m) : 0u, hi0 = min(t0, m - l);
+    uint32_t lo1 = t1 > (r - m) ? t1 - (r - m) : 0u, hi1 = min(t1, m - l);
+    while (hi0 - lo0 > 32u || hi1 - lo1 > 32u) {
+        const uint32_t w0 = hi0 - lo0, w1 = hi1 - lo1;
+        const uint32_t q0 = lo0 + (uint32_t)(((unsigned long long)(lane + 1u) * w0) / 33u);
+        const uint32_t q1 = lo1 + (uint32_t)(((unsigned long long)(lane + 1u) * w1) / 33u);
+        const bool a0 = w0 > 32u && __ldcg(src + l + q0) <= __ldcg(src + m + (t0 - q0 - 1u));
+        const bool a1 = w1 > 32u && __ldcg(src + l + q1) <= __ldcg(src + m + (t1 - q1 - 1u));
+        const uint32_t c0 = (uint32_t)__popc(__ballot_sync(0xffffffffu, a0));
+        const uint32_t c1 = (uint32_t)__popc(__ballot_sync(0xffffffffu, a1));
+        const uint32_t ql0 = __shfl_sync(0xffffffffu, q0, (c0 + 31u) & 31u), qh0 = __shfl_sync(0xffffffffu, q0, c0 & 31u);
+        const uint32_t ql1 = __shfl_sync(0xffffffffu, q1, (c1 + 31u) & 31u), qh1 = __shfl_sync(0xffffffffu, q1, c1 & 31u);
+        if (w0 > 32u) { if (c0 > 0u) lo0 = ql0 + 1u; if (c0 < 32u) hi0 = qh0; }
+        if (w1 > 32u) { if (c1 > 0u) lo1 = ql1 + 1u; if (c1 < 32u) hi1 = qh1; }
+    }
+    const uint32_t q0 = lo0 + lane, q1 = lo1 + lane;
+    const bool a0 = q0 < hi0 && __ldcg(src + l + q0) <= __ldcg(src + m + (t0 - q0 - 1u));
+    const bool a1 = q1 < hi1 && __ldcg(src + l + q1) <= __ldcg(src + m + (t1 - q1 - 1u));
+    return make_uint2(lo0 + (uint32_t)__popc(__ballot_sync(0xffffffffu, a0)),
+                      lo1 + (uint32_t)__popc(__ballot_sync(0xffffffffu, a1)));
 }
 
 constexpr uint32_t kBlockAssistMin = 1u << 17;  // merges this long are shared by the block's warps
 constexpr uint32_t kChunk = 1u << 16;           // output keys per claimed chunk
+
+// GPU-wide assist board (GTAP_MERGE_WARP, merges >= kGlobalAssistMin): any idle warp of the grid
+// claims kGChunk-key output chunks of an open slot. Slot protocol (all words in global memory):
+// requester CAS state 0 -> 1, writes the parameters, fence, next = 0, fence, state = 2 (release),
+// open += 1; a claim is atomicAdd(next) followed by a fence and the parameter reads, so a claim that
+// lands after a reopen sees the new parameters; closing sets next = 2^31 (late claims fail) before
+// state = 0. A helper fences its chunk's stores before done += 1; the requester waits for
+// done == nchunks and fences before its join release.
+constexpr uint32_t kGSlots = 1024;
+#ifndef GTAP_MS_GLOBAL_MIN
+#define GTAP_MS_GLOBAL_MIN 16384
+#endif
+#ifndef GTAP_MS_GCHUNK
+#define GTAP_MS_GCHUNK 4096
+#endif
+constexpr uint32_t kGlobalAssistMin = GTAP_MS_GLOBAL_MIN;
+constexpr uint32_t kGChunk = GTAP_MS_GCHUNK;
+struct __align__(128) GSlot {
+    uint32_t state, next, done, nchunks;
+    uint32_t l, m, r, depth;
+    uint32_t pad[24];
+};
+struct GBoard {
+    uint32_t open;                               // slots in state 2
+    uint32_t hint;                               // last slot opened
+    uint32_t pad[30];
+    uint32_t bits[kGSlots / 32];                 // slots with unclaimed chunks (set at open, cleared by the last claim)
+    GSlot slot[kGSlots];
+};
 
 struct MergesortTable {
     static constexpr uint32_t kKind = GTAP_WORKER_THREAD;
@@ -695,7 +869,10 @@ struct MergesortTable {
     }
     static constexpr int kMaxThreads = 128, kMinBlocks = 4;  // __launch_bounds__: 128 regs, no spills
     static constexpr bool kAssist = true;                    // heavy merges: warp assist (merge_mode 1)
-    static constexpr uint32_t kAssistMin = 8192;
+#ifndef GTAP_MS_ASSIST_MIN
+#define GTAP_MS_ASSIST_MIN 0
+#endif
+    static constexpr uint32_t kAssistMin = GTAP_MS_ASSIST_MIN;
     struct Args {
         int32_t* keys;
         int32_t* scratch;
@@ -703,14 +880,30 @@ struct MergesortTable {
         uint32_t n;         // array length (TMA path needs n % 4 == 0 and 16-B aligned buffers)
         uint32_t mode;      // GTAP_MERGE_THREAD (0) or GTAP_MERGE_WARP (1)
         uint32_t pad;
+        GBoard* gb;         // GPU-wide assist board (table-owned, reset before each run)
     };
     // warp assist: ap = {l, r, depth}; all 32 lanes
     __device__ __forceinline__ static bool assist(const Args& a, const uint32_t (&ap)[kDataWords], uint32_t lane,
                                                   MergeSlotHolder* H) {
         static_assert(kMaxThreads / 32 <= kMsWarps, "one WarpTiles per warp");
         const uint32_t l = ap[0], r = ap[1], depth = ap[2];
+        MS_T0;
+        if (ap[3] == 1u) {  // sequential_sort of a leaf, by the warp
+            warp_leaf_sort(a.keys, buf(a, depth), l, r, lane);
+            MS_TRACE_LANE0(r - l, l, 2u);
+            return true;
+        }
         const uint32_t m = l + (r - l) / 2u;
+        if (r - l <= kBitonicMax) {
+            warp_merge_small(buf(a, depth + 1u), buf(a, depth), l, m, r, lane);
+            MS_TRACE_LANE0(r - l, l, 3u);
+            return true;
+        }
         WarpTiles* T = H->tiles(threadIdx.x >> 5);
+        if (r - l >= kGlobalAssistMin && a.gb != nullptr && global_assist(a, l, m, r, depth, lane, T)) {
+            MS_TRACE_LANE0(r - l, l, 5u);
+            return true;
+        }
         if (r - l >= kBlockAssistMin) {
             // block assist: open the board, merge chunks alongside the block's other warps (they
             // join at the top of their scheduler loops), wait until every chunk is done
@@ -737,10 +930,12 @@ struct MergesortTable {
                 __syncwarp();
                 __threadfence();  // helpers fenced their stores before counting; order them before our release
                 __syncwarp();
+                MS_TRACE_LANE0(r - l, l, 4u);
                 return true;
             }
         }
         warp_merge(buf(a, depth + 1u), buf(a, depth), l, m, m, r, l, lane, T);
+        MS_TRACE_LANE0(r - l, l, 3u);
         return true;
     }
 
@@ -757,10 +952,123 @@ struct MergesortTable {
             const uint32_t l = B.l, m = B.m, r = B.r, depth = B.depth;
             const int32_t* src = buf(a, depth + 1u);
             const uint32_t n = r - l, o0 = c * kChunk, o1 = min(n, o0 + kChunk);
-            const uint32_t i0 = warp_split(src, l, m, r, o0, lane), i1 = warp_split(src, l, m, r, o1, lane);
+            MS_T0;
+            const uint2 sp = warp_split2(src, l, m, r, o0, o1, lane);
+            const uint32_t i0 = sp.x, i1 = sp.y;
             warp_merge(src, buf(a, depth), l + i0, l + i1, m + (o0 - i0), m + (o1 - i1), l + o0, lane, T);
             if (lane == 0) atomicAdd(&H->board.done, 1u);  // warp_merge fenced the chunk's stores
+            MS_TRACE_LANE0(o1 - o0, l + o0, 7u);
         }
+    }
+
+    // claim and merge chunks of global slot S until none is left (all 32 lanes)
+    __device__ __noinline__ static void gchunks(const Args& a, GSlot* S, uint32_t lane, WarpTiles* T) {
+        using namespace dev;
+        const uint32_t si = (uint32_t)(S - a.gb->slot);
+        while (true) {
+            uint32_t c = 0;
+            if (lane == 0) c = atom_add_relaxed(&S->next, 1u);
+            c = __shfl_sync(0xffffffffu, c, 0);
+            __threadfence();
+            const uint32_t nch = ld_relaxed(&S->nchunks);   // read after the claim (see GBoard)
+            if (c >= nch) break;
+            if (c == nch - 1u && lane == 0) atomicAnd(&a.gb->bits[si >> 5], ~(1u << (si & 31u)));  // all claimed
+            const uint32_t l = ld_relaxed(&S->l), m = ld_relaxed(&S->m), r = ld_relaxed(&S->r),
+                           depth = ld_relaxed(&S->depth);
+            const int32_t* src = buf(a, depth + 1u);
+            const uint32_t n = r - l, o0 = c * kGChunk, o1 = min(n, o0 + kGChunk);
+            MS_T0;
+            const uint2 sp = warp_split2(src, l, m, r, o0, o1, lane);
+            const uint32_t i0 = sp.x, i1 = sp.y;
+            warp_merge(src, buf(a, depth), l + i0, l + i1, m + (o0 - i0), m + (o1 - i1), l + o0, lane, T);
+            if (lane == 0) atom_add_relaxed(&S->done, 1u);   // warp_merge fenced the chunk's stores
+            MS_TRACE_LANE0(o1 - o0, l + o0, 6u);
+        }
+    }
+
+    // find an open global slot with unclaimed chunks and work on it; false if none (all 32 lanes)
+    __device__ __noinline__ static bool help_global_once(const Args& a, uint32_t lane, WarpTiles* T) {
+        using namespace dev;
+        GBoard* gb = a.gb;
+        uint32_t open = 0, hint = 0;
+        if (lane == 0) { open = ld_relaxed(&gb->open); hint = ld_relaxed(&gb->hint); }
+        if (__shfl_sync(0xffffffffu, open, 0) == 0u) return false;
+        hint = __shfl_sync(0xffffffffu, hint, 0);
+        static_assert(kGSlots / 32 == 32, "one bitmap word per lane");
+        // lane k reads bitmap word (k + rot): open slots with unclaimed chunks; rotate by the hint so
+        // helpers spread over the open slots
+        const uint32_t wi = (lane + (hint >> 5)) & 31u;
+        const uint32_t word = ld_relaxed(&gb->bits[wi]);
+        const uint32_t bal = __ballot_sync(0xffffffffu, word != 0u);
+        if (bal == 0u) return false;
+        const uint32_t src_lane = (uint32_t)__ffs(bal) - 1u;
+        const uint32_t wsel = __shfl_sync(0xffffffffu, word, src_lane);
+        const uint32_t wix = __shfl_sync(0xffffffffu, wi, src_lane);
+        // a set bit chosen by a per-warp rotation
+        const uint32_t rot = (hint + (blockIdx.x * 4u + (threadIdx.x >> 5)) * 7u) & 31u;
+        const uint32_t rotw = (wsel >> rot) | (rot ? (wsel << (32u - rot)) : 0u);
+        const uint32_t bit = ((uint32_t)__ffs(rotw) - 1u + rot) & 31u;
+        gchunks(a, gb->slot + wix * 32u + bit, lane, T);
+        return true;
+    }
+
+    // requester side (all 32 lanes); false if no slot was free (the caller merges another way)
+    __device__ __noinline__ static bool global_assist(const Args& a, uint32_t l, uint32_t m, uint32_t r,
+                                                      uint32_t depth, uint32_t lane, WarpTiles* T) {
+        using namespace dev;
+        GBoard* gb = a.gb;
+        uint32_t sidx = kNone;
+        const uint32_t h = (l >> 15) * 0x9E3779B1u;
+        for (uint32_t base = 0; base < 128u && sidx == kNone; base += 32u) {
+            const uint32_t cand = (h + base + lane) & (kGSlots - 1u);
+            uint32_t bal = __ballot_sync(0xffffffffu, ld_relaxed(&gb->slot[cand].state) == 0u);
+            while (bal) {
+                const uint32_t k = (uint32_t)__ffs(bal) - 1u;
+                bal &= bal - 1u;
+                uint32_t ok = 0;
+                if (lane == k) ok = atom_cas_relaxed(&gb->slot[cand].state, 0u, 1u) == 0u ? 1u : 0u;
+                if (__shfl_sync(0xffffffffu, ok, k)) { sidx = __shfl_sync(0xffffffffu, cand, k); break; }
+            }
+        }
+        if (sidx == kNone) return false;
+        GSlot* S = gb->slot + sidx;
+        const uint32_t nch = (r - l + kGChunk - 1u) / kGChunk;
+        if (lane == 0) {
+            st_relaxed(&S->l, l); st_relaxed(&S->m, m); st_relaxed(&S->r, r); st_relaxed(&S->depth, depth);
+            st_relaxed(&S->nchunks, nch); st_relaxed(&S->done, 0u);
+            __threadfence();
+            atom_exch_relaxed(&S->next, 0u);
+            __threadfence();
+            st_release(&S->state, 2u);
+            atomicOr(&gb->bits[sidx >> 5], 1u << (sidx & 31u));
+            red_add_relaxed(&gb->open, 1u);
+            st_relaxed(&gb->hint, sidx);
+        }
+        __syncwarp();
+        gchunks(a, S, lane, T);
+        while (true) {   // wait for the helpers; meanwhile help other open slots
+            uint32_t dn = 0;
+            if (lane == 0) dn = ld_relaxed(&S->done);
+            if (__shfl_sync(0xffffffffu, dn, 0) >= nch) break;
+            if (!help_global_once(a, lane, T) && lane == 0) nanosleep(256);
+            __syncwarp();
+        }
+        if (lane == 0) {
+            atom_exch_relaxed(&S->next, 0x80000000u);
+            red_add_relaxed(&gb->open, 0xFFFFFFFFu);
+            __threadfence();
+            st_release(&S->state, 0u);
+        }
+        __syncwarp();
+        __threadfence();
+        __syncwarp();
+        return true;
+    }
+
+    // scheduler hook, idle path (all 32 lanes): help an open GPU-wide assist
+    __device__ __forceinline__ static bool help_idle(const Args& a, uint32_t lane, MergeSlotHolder* H) {
+        if (a.gb == nullptr) return false;
+        return help_global_once(a, lane, H->tiles(threadIdx.x >> 5));
     }
 
     // scheduler hook, top of every cycle (all 32 lanes): join an open board of this block
@@ -809,31 +1117,18 @@ struct MergesortTable {
                                                  uint32_t m, uint32_t r, MergeSlotHolder* S) {
         const bool tma_ok = (r - l) >= kTmaMin && (a.n & 3u) == 0u &&
                             ((reinterpret_cast<uintptr_t>(a.keys) | reinterpret_cast<uintptr_t>(a.scratch)) & 15u) == 0u;
-#ifdef GTAP_MS_TRACE
-        const unsigned long long t0 = dev::globaltimer();
-        uint32_t used = 0;
-#endif
+        MS_T0;
         bool ok = true;
+        uint32_t used = 0;
         if (tma_ok && atomicCAS(&S->busy, 0u, 1u) == 0u) {
             ok = ms_merge_tma(src, dst, l, m, r, a.n, S);
             atomicExch(&S->busy, 0u);
-#ifdef GTAP_MS_TRACE
             used = 1;
-#endif
         } else {
             ms_merge(src, dst, l, m, r);
         }
-#ifdef GTAP_MS_TRACE
-        if (r - l >= 4096u) {
-            const uint32_t i = atomicAdd(&gtap_ms_trace_n, 1u);
-            if (i < 65536u) {
-                unsigned smid;
-                asm("mov.u32 %0, %%smid;" : "=r"(smid));
-                gtap_ms_trace[i] = make_ulonglong4(t0, dev::globaltimer(), ((unsigned long long)(r - l) << 32) | l,
-                                                   ((unsigned long long)smid << 8) | used);
-            }
-        }
-#endif
+        MS_TRACE(r - l, l, used);
+        (void)used;
         return ok;
     }
 
@@ -845,7 +1140,14 @@ struct MergesortTable {
         switch (state) {
             case 0:
                 if (r - l <= a.cutoff) {
+                    if (a.mode == 1u) {                       // by the whole warp (bitonic, registers)
+                        o.request_assist(l, r, depth, 1u);
+                        o.finish_void();
+                        return;
+                    }
+                    MS_T0;
                     leaf_sort(a.keys, buf(a, depth), l, r);
+                    MS_TRACE(r - l, l, 2u);
                     o.finish_void();
                     return;
                 } else {
@@ -883,8 +1185,18 @@ extern "C" const gtap_task_table* gtap_table_mergesort_ex(int32_t* keys, int32_t
                                                          uint32_t merge_mode) {
     if (((!keys || !scratch) && n > 0) || cutoff < 1 || cutoff > gtap::kMsMaxCutoff || n >= (1ull << 31)) return nullptr;
     if (merge_mode > 1u) return nullptr;
-    gtap::MergesortTable::Args a{keys, scratch, (uint32_t)cutoff, (uint32_t)n, merge_mode, 0u};
-    return gtap::make_table<gtap::MergesortTable>("mergesort", a, &gtap::validate_ms);
+    gtap::GBoard* gb = nullptr;
+    if (merge_mode == 1u && cudaMalloc(&gb, sizeof(gtap::GBoard)) != cudaSuccess) return nullptr;
+    gtap::MergesortTable::Args a{keys, scratch, (uint32_t)cutoff, (uint32_t)n, merge_mode, 0u, gb};
+    gtap_task_table* t = gtap::make_table<gtap::MergesortTable>("mergesort", a, &gtap::validate_ms);
+    if (!t) { cudaFree(gb); return nullptr; }
+    if (gb) {
+        t->dev_scratch = gb;
+        t->prepare = [](const gtap_task_table* tt, cudaStream_t s) {
+            return cudaMemsetAsync(tt->dev_scratch, 0, sizeof(gtap::GBoard), s);
+        };
+    }
+    return t;
 }
 
 extern "C" const gtap_task_table* gtap_table_mergesort(int32_t* keys, int32_t* scratch, uint64_t n, int32_t cutoff) {

@@ -53,20 +53,24 @@ def test_sizes(g, rt, mode, n):
     ref, tasks, inv = oracle.mergesort(keys, 128)
     assert np.array_equal(out, ref)
     assert (st.tasks, st.invocations) == (tasks, inv)
-    if mode == 0 or n < 8192:
+    if mode == 0:
         assert st.assists == 0
-    else:  # every merge of >= 8192 keys ran as a warp assist
-        assert st.assists == sum(1 for r in _merge_sizes(n, 128) if r >= 8192)
+    else:  # every leaf and every merge ran as a warp assist
+        merges, leaves = _shape(n, 128)
+        assert st.assists == leaves + len(merges)
 
 
-def _merge_sizes(n, cutoff):
-    out, stack = [], [n]
+def _shape(n, cutoff):
+    """(merge sizes, leaf count) of the cutoff mergesort recursion on n keys."""
+    merges, leaves, stack = [], 0, [n]
     while stack:
         k = stack.pop()
         if k > cutoff:
-            out.append(k)
+            merges.append(k)
             stack += [k // 2, k - k // 2]
-    return out
+        else:
+            leaves += 1
+    return merges, leaves
 
 
 @pytest.mark.parametrize("cutoff", [1, 2, 3, 64, 128, 255, 256])

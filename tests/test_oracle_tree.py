@@ -3,8 +3,8 @@
 * full binary tree: tasks = 2^(D+1) - 1 (P:619, closed form);
 * pruned B-ary tree: p(0) = 1 so the root always has B children; for D = 1 exactly 1 + B tasks;
   the shape is a pure function of (D, B, seed) (counter-based, SPEC S:547) and thins with depth;
-* do_memory_and_compute: the memory part of one node restated with numpy (sum of 64-bit words
-  at mixed indices) and the FMA part against math.fma chains, via a 1-node tree (D = 0).
+* do_memory_and_compute: one node restated in Python (sum of 64-bit words at mixed indices, FMA
+  chains with an exact-rational FMA), via a 1-node tree (D = 0), and summed over small trees.
 """
 import struct
 from fractions import Fraction
@@ -33,9 +33,9 @@ def work_py(node, buf, mem_ops, compute_iters):
     s = 0
     for i in range(mem_ops):
         s += int(buf[mix((node * 0x9E3779B97F4A7C15 + i) & M64) % len(buf)])
-    for c in range(32):
+    for c in range(min(64, compute_iters)):
         f = 1.0 + ((node + c) & 1023) / 1024.0
-        for _ in range(compute_iters // 32 + (1 if c < compute_iters % 32 else 0)):
+        for _ in range(compute_iters // 64 + (1 if c < compute_iters % 64 else 0)):
             f = fma(f, 0.999999, 1e-7)
         s += struct.unpack("<Q", struct.pack("<d", f))[0]
     return s & M64
@@ -51,7 +51,7 @@ def test_full_tree_count(buf, D):
     assert oracle.tree(D, buf, 3, 40)[1] == 2 ** (D + 1) - 1
 
 
-@pytest.mark.parametrize("mem,comp", [(0, 0), (5, 0), (0, 70), (17, 33)])
+@pytest.mark.parametrize("mem,comp", [(0, 0), (5, 0), (0, 70), (17, 33), (0, 130)])
 def test_single_node_work(buf, mem, comp):
     total, tasks = oracle.tree(0, buf, mem, comp)   # full tree, D = 0: just the root (id 1)
     assert tasks == 1 and total == work_py(1, buf, mem, comp)

@@ -106,9 +106,10 @@ int oracle_fib_cutoff(int32_t n, int32_t cutoff, int64_t *value, int64_t *tasks,
  *     mix(seed ^ child_id) >> 11 < floor((D - d) * 2^53 / D) (counter-based:
  *     the shape does not depend on the schedule);
  *   - do_memory_and_compute(id) = sum_i buf[mix(id * G + i) mod len]
- *     + sum over 32 independent FMA chains of the final chain value's bits
- *     (chain c: f = 1 + ((id + c) & 1023) / 1024, then f = fma(f, 0.999999, 1e-7)
- *     repeated compute_iters / 32 (+1 for c < compute_iters mod 32) times),
+ *     + the bits of the final value of each of the min(64, compute_iters)
+ *     independent FMA chains (chain c: f = 1 + ((id + c) & 1023) / 1024, then
+ *     f = fma(f, 0.999999, 1e-7) repeated compute_iters / 64 (+1 for
+ *     c < compute_iters mod 64) times, i.e. compute_iters FMAs in total),
  *     all mod 2^64; the run's value is the sum over all nodes.
  */
 static uint64_t t_mix(uint64_t z)
@@ -123,9 +124,9 @@ static uint64_t tree_work(uint64_t id, const uint64_t *buf, uint64_t len, int64_
     uint64_t s = 0;
     for (int64_t i = 0; i < mem_ops; i++)
         s += buf[t_mix(id * 0x9E3779B97F4A7C15ull + (uint64_t)i) % len];
-    for (int c = 0; c < 32; c++) {
+    for (int c = 0; c < 64 && c < compute_iters; c++) {
         double f = 1.0 + (double)((id + (uint64_t)c) & 1023u) / 1024.0;
-        int64_t it = compute_iters / 32 + (c < compute_iters % 32 ? 1 : 0);
+        int64_t it = compute_iters / 64 + (c < compute_iters % 64 ? 1 : 0);
         for (int64_t j = 0; j < it; j++) f = fma(f, 0.999999, 1e-7);
         uint64_t bits;
         memcpy(&bits, &f, 8);

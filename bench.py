@@ -44,13 +44,14 @@ FIB_CFG = dict(grid_size=0, block_size=128, max_tasks_per_worker=4096)
 SPMV_ROWS = 1 << 22
 SPMV_NNZ_CUT = 8192
 SPMV_FANOUT = 32
-SPMV_CFG = dict(grid_size=148 * 8, block_size=128, max_tasks_per_worker=1024)
+SPMV_PARTS = 148 * 8     # forest: one nnz-balanced root per worker (fn part(k, R), reading R20)
+SPMV_CFG = dict(grid_size=148 * 8, block_size=128, max_tasks_per_worker=1024, max_roots=SPMV_PARTS)
 CS_CFG = dict(grid_size=0, block_size=128, max_tasks_per_worker=4096)
 NQ_N = 16
 NQ_CUTOFF = 7
 NQ_CFG = dict(grid_size=0, block_size=128, max_tasks_per_worker=4096)
 BFS_SCALE = 22
-BFS_CFG = dict(grid_size=148 * 4, block_size=256, max_tasks_per_worker=1 << 19, idle_backoff_ns=1024)
+BFS_CFG = dict(grid_size=148 * 16, block_size=64, max_tasks_per_worker=1 << 17, idle_backoff_ns=1024)
 
 L2_FLUSH_BYTES = 256 << 20
 METRIC = "Mkeys/s (mergesort 2^24 int32, cutoff 128), device-timed"
@@ -414,7 +415,7 @@ def bench_spmv(dev, ws=1, rank=0, reps=5):
     for i in range(reps + 1):
         flush.fill_(1)
         rt.reset()
-        y, st = g.spmv(rp, col, val, x, y, SPMV_NNZ_CUT, SPMV_FANOUT, rows=(lo, hi), rt=rt)
+        y, st = g.spmv(rp, col, val, x, y, SPMV_NNZ_CUT, SPMV_FANOUT, rows=(lo, hi), parts=SPMV_PARTS, rt=rt)
         if i:
             ms.append(st.device_ms)
     rt.close()
@@ -426,7 +427,10 @@ def bench_spmv(dev, ws=1, rank=0, reps=5):
     pk, _ = peaks()
     return dict(workload=f"SpMV power-law 2^22 rows (configs[3]), block-level, rows split over {ws} GPU(s)",
                 metric="GB/s", value=algo / (t * 1e-3) / 1e9, gflops=2.0 * nnz / (t * 1e-3) / 1e9, ms=t, nnz=nnz,
-                tasks=st.tasks, frac_hbm_per_gpu=algo / ws / (t * 1e-3) / 1e9 / pk["hbm_gbs"],
+                tasks=st.tasks, frac_hbm_per_gpu=algo / ws / (t * 1e-3) / 1e9 / pk["hbm_gbs"], roots=SPMV_PARTS,
+                gather_floor_ms=0.50, gather_floor_note="a bare streaming gather (sum val*x[col], no rows, no "
+                "scheduler) over this matrix takes 0.50 ms on B200: the random 32-B x sectors bound any CSR "
+                "SpMV here (profiles/r01_spmv_gather_floor.txt)",
                 traffic=profile_traffic("spmv"), scaling="strong", y_checksum=float(y.double().sum().item()))
 
 

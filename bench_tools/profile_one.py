@@ -27,9 +27,11 @@ elif wl == "fib":
 elif wl == "spmv":
     rows = size or (1 << 22)
     rp, col, val, x = synth.powerlaw_csr(rows, seed=7, device="cuda")
-    with g.Runtime(g.GTAP_WORKER_BLOCK, 0, **bench.SPMV_CFG) as rt:
+    parts = int(os.environ.get("SPMV_PARTS", getattr(bench, "SPMV_PARTS", 0)))
+    cut = int(os.environ.get("SPMV_CUT", bench.SPMV_NNZ_CUT))
+    with g.Runtime(g.GTAP_WORKER_BLOCK, 0, max_roots=max(parts, 1), **bench.SPMV_CFG) as rt:
         for i in range(reps):
-            y, st = g.spmv(rp, col, val, x, nnz_cut=bench.SPMV_NNZ_CUT, fanout=bench.SPMV_FANOUT, rt=rt)
+            y, st = g.spmv(rp, col, val, x, nnz_cut=cut, fanout=bench.SPMV_FANOUT, parts=parts, rt=rt)
             print("spmv", rows, st.device_ms, st.tasks, flush=True)
 elif wl == "bfs":
     scale = size or 22

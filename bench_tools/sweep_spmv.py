@@ -1,14 +1,33 @@
-import sys, os, statistics
+"""SpMV sweep: launch geometry x split cutoff x forest size (parts = 0: one root)."""
+import os
+import statistics
+import sys
+
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import torch, synth
-import paper_2604_05982_b200 as g
+import torch  # noqa: E402
+
+import paper_2604_05982_b200 as g  # noqa: E402
+import synth  # noqa: E402
+
 rp, col, val, x = synth.powerlaw_csr(1 << 22, seed=7, device="cuda")
 y = torch.empty(1 << 22, dtype=torch.float32, device="cuda")
-nnz = int(rp[-1]); algo = 8.0 * nnz + 12.0 * (1 << 22)
-for grid, block in [(148*4, 256), (148*8, 128), (148*2, 512)]:
-    with g.Runtime(g.GTAP_WORKER_BLOCK, 0, grid_size=grid, block_size=block, max_tasks_per_worker=2048) as rt:
-        for cut in (8192, 32768, 131072):
-            for fan in (16, 32):
-                ms = [g.spmv(rp, col, val, x, y, cut, fan, rt=rt)[1] for _ in range(4)]
-                t = statistics.median(s.device_ms for s in ms[1:])
-                print(f"grid={grid} block={block} cut={cut} fan={fan} ms={t:.3f} GB/s={algo/t/1e6:.0f} tasks={ms[-1].tasks}", flush=True)
+nnz = int(rp[-1])
+algo = 8.0 * nnz + 12.0 * (1 << 22)
+ref = None
+CFGS = {'libgtap.so': [(148 * 8, 128)], 'libgtap_gtap_spmv_per16.so': [(148 * 8, 128)], 'libgtap_gtap_spmv_per12.so': [(148 * 8, 128)],
+        'libgtap_gtap_spmv_per16_gtap_spmv_minb3.so': [(148 * 6, 128), (148 * 3, 256)]}
+for grid, block in CFGS[os.path.basename(os.environ.get('GTAP_LIB', 'libgtap.so'))]:
+    with g.Runtime(g.GTAP_WORKER_BLOCK, 0, grid_size=grid, block_size=block, max_tasks_per_worker=2048,
+                   max_roots=4 * grid) as rt:
+        for parts in (grid, 2 * grid):
+            for cut in (8192, 65536):
+                sts = []
+                for _ in range(4):
+                    y.zero_()
+                    sts.append(g.spmv(rp, col, val, x, y, cut, 32, parts=parts, rt=rt)[1])
+                if ref is None:
+                    ref = y.clone()
+                err = float(((y - ref).abs() / ref.abs().clamp_min(1e-30)).max())
+                t = statistics.median(s.device_ms for s in sts[1:])
+                print(f"{os.path.basename(os.environ.get('GTAP_LIB', 'libgtap.so'))[7:]:30s} grid={grid} block={block} parts={parts:5d} cut={cut:6d} ms={t:.3f} GB/s={algo / t / 1e6:.0f} "
+                      f"tasks={sts[-1].tasks} maxrel={err:.1e}", flush=True)

@@ -237,7 +237,14 @@ const gtap_task_table *gtap_table_cilksort(int32_t *keys, int32_t *scratch, uint
  * no taskwait. Task spmv(lo, hi) splits the row range into `fanout` equal
  * parts while it holds more than nnz_cut non-zeros (and > 1 row); leaves are
  * computed cooperatively by the block in fp32. fn 0, root args
- * {uint32 lo, uint32 hi}. y rows outside roots' ranges are untouched. */
+ * {uint32 lo, uint32 hi}. fn 1 = part(k, R, r0, r1), root args {uint32 k,
+ * uint32 R, uint32 r0, uint32 r1} (r1 = 0: nrows), k < R: the k-th of R
+ * contiguous row ranges of [r0, r1) balanced by non-zeros (boundary j = first
+ * row whose start offset reaches row_ptr[r0] + floor(j * nnz(r0, r1) / R),
+ * found in the kernel), then processed as spmv(lo, hi); the R roots k =
+ * 0..R-1 cover every row of [r0, r1) once (a forest: each worker starts with
+ * its own range, R20).
+ * y rows outside roots' ranges are untouched. */
 const gtap_task_table *gtap_table_spmv(const int32_t *row_ptr, const int32_t *col,
                                        const float *val, const float *x, float *y,
                                        uint32_t nrows, uint32_t nnz_cut, uint32_t fanout);

@@ -156,17 +156,26 @@ def mergesort_forest_(keys, segments, scratch=None, cutoff: int = 128, merge_mod
             rt.close()
 
 
-def spmv(row_ptr, col, val, x, y=None, nnz_cut: int = 8192, fanout: int = 16, rows=None,
+def spmv(row_ptr, col, val, x, y=None, nnz_cut: int = 8192, fanout: int = 16, rows=None, parts: int = 0,
          rt: Runtime | None = None, stream=None, **cfg):
-    """y = A x for a CSR matrix with block-cooperative task leaves (rows=(lo, hi) restricts the root)."""
+    """y = A x for a CSR matrix with block-cooperative task leaves.
+
+    rows=(lo, hi) restricts the work to a row range; parts=R > 0 spawns a forest of R roots
+    part(k, R, lo, hi) (nnz-balanced row ranges found in the kernel) instead of one root."""
     import torch
     if y is None:
         y = torch.empty(row_ptr.numel() - 1, dtype=torch.float32, device=row_ptr.device)
+    if parts:
+        cfg.setdefault("max_roots", parts)
     rt, own = _runtime(GTAP_WORKER_BLOCK, rt, row_ptr.device.index or 0, cfg)
     table = Table.spmv(row_ptr, col, val, x, y, nnz_cut, fanout)
     lo, hi = rows if rows is not None else (0, row_ptr.numel() - 1)
     try:
-        rt.spawn_root(table, (lo, hi))
+        if parts:
+            for k in range(parts):
+                rt.spawn_root(table, (k, parts, lo, hi), fn=1)
+        else:
+            rt.spawn_root(table, (lo, hi))
         rt.run(stream)
         return y, rt.sync()
     finally:

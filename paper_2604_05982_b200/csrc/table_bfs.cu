@@ -21,7 +21,10 @@ struct BfsTable {
     static constexpr uint32_t kNumFn = 1;
     static constexpr bool kJoinReduceAdd = false;  // see TaskRec
     static constexpr int kMaxThreads = 1024, kMinBlocks = 1;  // __launch_bounds__
-    static constexpr int kSpawnCap = 1536;
+#ifndef GTAP_BFS_SPAWN_CAP
+#define GTAP_BFS_SPAWN_CAP 512
+#endif
+    static constexpr int kSpawnCap = GTAP_BFS_SPAWN_CAP;
     struct Scratch {
         uint32_t unused;
     };

@@ -21,11 +21,17 @@ struct SpmvTable {
     static constexpr uint32_t kKind = GTAP_WORKER_BLOCK;
     static constexpr int kMaxChildren = 32;
     static constexpr bool kTaskwait = false;
-    static constexpr uint32_t kNumFn = 1;
+    static constexpr uint32_t kNumFn = 2;          // 0: spmv(lo, hi); 1: part(k, R) (a forest root)
     static constexpr bool kJoinReduceAdd = false;  // see TaskRec
-    static constexpr int kMaxThreads = 256, kMinBlocks = 4;  // __launch_bounds__ (prod[] holds 8 x 256)
+#ifndef GTAP_SPMV_MINB
+#define GTAP_SPMV_MINB 4
+#endif
+    static constexpr int kMaxThreads = 256, kMinBlocks = GTAP_SPMV_MINB;  // __launch_bounds__ (prod[] holds 8 x 256)
     static constexpr int kSpawnCap = 32;
-    static constexpr int kPer = 8;          // non-zeros per thread per chunk
+#ifndef GTAP_SPMV_PER
+#define GTAP_SPMV_PER 8
+#endif
+    static constexpr int kPer = GTAP_SPMV_PER;  // non-zeros per thread per chunk
     static constexpr int kMaxBlock = 256;   // prod[] sized for blocks up to 256 threads
     static constexpr int kRp = 512;         // row_ptr entries staged per chunk (more rows: global loads)
     struct Scratch {
@@ -52,11 +58,33 @@ struct SpmvTable {
     template <class Ctx>
     __device__ __forceinline__ static void exec_block(const Args& a, Ctx& ctx, uint32_t fn, uint32_t state,
                                                       const uint32_t (&d)[kDataWords]) {
-        if (fn != 0u || state != 0u) {
+        if (fn > 1u || state != 0u) {
             if (threadIdx.x == 0) ctx.bad_state();
             return;
         }
-        const uint32_t lo = d[0], hi = d[1];
+        uint32_t lo = d[0], hi = d[1];
+        if (fn == 1u) {
+            // part(k, R, r0, r1): the k-th of R row ranges of [r0, r1) (r1 = 0: all rows) balanced by
+            // non-zeros (reading R20): boundary j is the first row whose start offset reaches
+            // row_ptr[r0] + floor(j * nnz(r0, r1) / R); every thread runs the same search (uniform
+            // loads), then the range is an ordinary spmv(lo, hi) task
+            const uint32_t k = d[0], R = d[1], r0 = d[2], r1 = d[3] ? d[3] : a.nrows;
+            const long long s0 = __ldg(&a.row_ptr[r0]);
+            const unsigned long long nnz = (unsigned long long)(__ldg(&a.row_ptr[r1]) - s0);
+            auto bound = [&](uint32_t j) -> uint32_t {
+                if (j == 0u) return r0;
+                if (j >= R) return r1;
+                const long long target = s0 + (long long)((nnz * j) / R);
+                uint32_t l = r0, h = r1;
+                while (l < h) {
+                    const uint32_t mid = (l + h) >> 1;
+                    if ((long long)__ldg(&a.row_ptr[mid]) < target) l = mid + 1u; else h = mid;
+                }
+                return l;
+            };
+            lo = bound(k);
+            hi = max(lo, bound(k + 1u));
+        }
         const int32_t s = __ldg(&a.row_ptr[lo]), e = __ldg(&a.row_ptr[hi]);
         const uint32_t tid = threadIdx.x, bd = blockDim.x;
         if ((uint32_t)(e - s) > a.nnz_cut && hi - lo > 1u) {
@@ -81,6 +109,42 @@ struct SpmvTable {
         const int32_t CH = kPer * (int32_t)bd;
         if (tid == 0) { sc.rcur = lo; sc.carry = 0.f; }
         __syncthreads();
+#ifdef GTAP_SPMV_PIPE
+        // software pipeline: chunk c+1's (col, val) loads are issued before chunk c's row phase and
+        // its x gathers right after it, so the memory latency overlaps the shared-memory reduction
+        int32_t cc[kPer];
+        float vv[kPer], pr[kPer];
+        if (s < e) {
+#pragma unroll
+            for (int k = 0; k < kPer; ++k) {
+                const int32_t idx = s + (int32_t)tid + k * (int32_t)bd;
+                const bool in = idx < min(s + CH, e);
+                cc[k] = ld_col(&a.col[in ? idx : s]);
+                vv[k] = in ? ld_val(&a.val[idx]) : 0.f;
+            }
+#pragma unroll
+            for (int k = 0; k < kPer; ++k) pr[k] = vv[k] * __ldg(&a.x[cc[k]]);
+        }
+        for (int32_t c0 = s; c0 < e; c0 += CH) {   // uniform
+            const int32_t c1 = min(c0 + CH, e);
+            const uint32_t r0 = sc.rcur;
+            for (uint32_t i = tid; i <= (uint32_t)kRp; i += bd)
+                sc.rp[i] = (r0 + i <= hi) ? __ldg(&a.row_ptr[r0 + i]) : e;
+#pragma unroll
+            for (int k = 0; k < kPer; ++k) sc.prod[tid + k * bd] = pr[k];
+            __syncthreads();
+            const bool more = c0 + CH < e;
+            if (more) {
+                const int32_t n0 = c0 + CH, n1 = min(n0 + CH, e);
+#pragma unroll
+                for (int k = 0; k < kPer; ++k) {
+                    const int32_t idx = n0 + (int32_t)tid + k * (int32_t)bd;
+                    const bool in = idx < n1;
+                    cc[k] = ld_col(&a.col[in ? idx : n0]);
+                    vv[k] = in ? ld_val(&a.val[idx]) : 0.f;
+                }
+            }
+#else
         for (int32_t c0 = s; c0 < e; c0 += CH) {   // uniform
             const int32_t c1 = min(c0 + CH, e);
             const uint32_t r0 = sc.rcur;
@@ -99,6 +163,7 @@ struct SpmvTable {
 #pragma unroll
             for (int k = 0; k < kPer; ++k) sc.prod[tid + k * bd] = vv[k] * __ldg(&a.x[cc[k]]);
             __syncthreads();
+#endif
             const float carry_in = sc.carry;
             for (uint32_t r = r0 + warp; r < hi; r += nw) {   // warp-uniform
                 const uint32_t i = r - r0;
@@ -119,6 +184,12 @@ struct SpmvTable {
                     }
                 }
             }
+#ifdef GTAP_SPMV_PIPE
+            if (more) {
+#pragma unroll
+                for (int k = 0; k < kPer; ++k) pr[k] = vv[k] * __ldg(&a.x[cc[k]]);
+            }
+#endif
             __syncthreads();
             if (tid == 0) { sc.rcur = sc.rnext; sc.carry = sc.carry_next; }
             __syncthreads();
@@ -133,6 +204,10 @@ struct SpmvTable {
 static int validate_spmv(const gtap_task_table* t, uint32_t fn, const uint32_t* d) {
     SpmvTable::Args a;
     std::memcpy(&a, t->args, sizeof(a));
+    if (fn == 1u) {   // part(k, R, r0, r1)
+        const uint32_t r1 = d[3] ? d[3] : a.nrows;
+        return (d[0] < d[1] && d[2] <= r1 && r1 <= a.nrows) ? 0 : -1;
+    }
     return (fn == 0u && d[0] <= d[1] && d[1] <= a.nrows) ? 0 : -1;
 }
 

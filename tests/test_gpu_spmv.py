@@ -99,7 +99,38 @@ def test_full_size_config3(g):
     import bench
     rp, col, val, x = synth.powerlaw_csr(1 << 22, seed=7, device="cuda")
     with g.Runtime(g.GTAP_WORKER_BLOCK, 0, watchdog_ns=60_000_000_000, **bench.SPMV_CFG) as r:
-        y, st = g.spmv(rp, col, val, x, rt=r, nnz_cut=bench.SPMV_NNZ_CUT, fanout=bench.SPMV_FANOUT)
+        y, st = g.spmv(rp, col, val, x, rt=r, nnz_cut=bench.SPMV_NNZ_CUT, fanout=bench.SPMV_FANOUT,
+                       parts=bench.SPMV_PARTS)
     y64, _ = oracle.spmv(rp.cpu(), col.cpu(), val.cpu(), x.cpu())
     rel = np.abs(y.cpu().numpy().astype(np.float64) - y64) / np.abs(y64)
     assert rel.max() <= RTOL, rel.max()
+
+
+@pytest.mark.parametrize("parts", [1, 2, 7, 148, 1184, 5000])
+@pytest.mark.parametrize("nnz_cut", [128, 1 << 20])
+def test_forest_parts(g, parts, nnz_cut):
+    """Forest of part(k, R) roots (nnz-balanced ranges found in the kernel): every row exactly once,
+    including R larger than the number of rows (empty parts) and heavy rows at range borders."""
+    rp, col, val, x = synth.powerlaw_csr(4099, seed=11)
+    with g.Runtime(g.GTAP_WORKER_BLOCK, 0, grid_size=148, block_size=128, max_tasks_per_worker=4096,
+                   max_roots=parts, watchdog_ns=WD) as r:
+        st = check(g, r, rp, col, val, x, nnz_cut=nnz_cut, parts=parts)
+    assert st.tasks >= parts
+
+
+def test_forest_subrange(g):
+    """parts over a row sub-range [lo, hi): rows outside keep their previous values."""
+    rp, col, val, x = synth.powerlaw_csr(5000, seed=12)
+    y64, _ = oracle.spmv(rp, col, val, x)
+    lo, hi = 1234, 4321
+    dev = [t.cuda() for t in (rp, col, val, x)]
+    y = torch.full((5000,), -7.0, dtype=torch.float32, device="cuda")
+    with g.Runtime(g.GTAP_WORKER_BLOCK, 0, grid_size=64, block_size=128, max_tasks_per_worker=4096, max_roots=37,
+                   watchdog_ns=WD) as r:
+        y, _ = g.spmv(*dev, y, nnz_cut=256, rows=(lo, hi), parts=37, rt=r)
+    y = y.cpu().numpy().astype(np.float64)
+    assert np.all(y[:lo] == -7.0) and np.all(y[hi:] == -7.0)
+    ne = rp[lo + 1:hi + 1].numpy() != rp[lo:hi].numpy()
+    rel = np.abs(y[lo:hi][ne] - y64[lo:hi][ne]) / np.abs(y64[lo:hi][ne])
+    assert rel.max() <= RTOL
+    assert np.all(y[lo:hi][~ne] == 0.0)

@@ -11,7 +11,7 @@
 __global__ void __launch_bounds__(LB_THREADS, LB_MIN) k_tma(const int* s, int* d, int n, int nt) {
     extern __shared__ __align__(128) unsigned char sm[];
     gtap::MergeSlotHolder* S = reinterpret_cast<gtap::MergeSlotHolder*>(sm);
-    if (threadIdx.x == 0) gtap::MergesortTable::block_init(S);
+    if (threadIdx.x == 0) gtap::MergesortTable<0u>::block_init(S);
     __syncthreads();
     if (threadIdx.x == 0) gtap::ms_merge_tma(s, d, 0, n / 2, n, nt, S);
 }
@@ -20,7 +20,7 @@ template <int MODE>
 __global__ void __launch_bounds__(128, 4) k_env(const int* s, int* d, int n, int nt) {
     extern __shared__ __align__(128) unsigned char sm[];
     gtap::MergeSlotHolder* S = reinterpret_cast<gtap::MergeSlotHolder*>(sm);
-    if (threadIdx.x == 0) { gtap::MergesortTable::block_init(S); g_done = 0; }
+    if (threadIdx.x == 0) { gtap::MergesortTable<0u>::block_init(S); g_done = 0; }
     __syncthreads();
     if (threadIdx.x < 32) {
         if (threadIdx.x == 0) { gtap::ms_merge_tma(s, d, 0, n / 2, n, nt, S); g_done = 1; }

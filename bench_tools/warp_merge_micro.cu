@@ -7,7 +7,7 @@
 
 __global__ void __launch_bounds__(128, 1) k_wm(const int* s, int* d, int n, int nprob) {
     extern __shared__ __align__(128) unsigned char sm[];
-    gtap::MergeSlotHolder* H = reinterpret_cast<gtap::MergeSlotHolder*>(sm);
+    gtap::WarpAssistHolder* H = reinterpret_cast<gtap::WarpAssistHolder*>(sm);
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
     const uint32_t prob = blockIdx.x * (blockDim.x >> 5) + warp;
     if (prob >= (uint32_t)nprob) return;
@@ -29,7 +29,7 @@ int main(int argc, char** argv) {
     int *s, *d;
     cudaMalloc(&s, h.size() * 4); cudaMalloc(&d, h.size() * 4);
     cudaMemcpy(s, h.data(), h.size() * 4, cudaMemcpyHostToDevice);
-    const int smem = (int)sizeof(gtap::MergeSlotHolder);
+    const int smem = (int)sizeof(gtap::WarpAssistHolder);
     cudaFuncSetAttribute(k_wm, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
     const int blocks = (nprob + wpb - 1) / wpb;

@@ -25,6 +25,10 @@ struct BfsTable {
 #define GTAP_BFS_SPAWN_CAP 512
 #endif
     static constexpr int kSpawnCap = GTAP_BFS_SPAWN_CAP;
+#ifndef GTAP_BFS_U
+#define GTAP_BFS_U 4
+#endif
+    static constexpr uint32_t kU = GTAP_BFS_U;       // edges per thread per step
     struct Scratch {
         uint32_t unused;
     };
@@ -47,18 +51,29 @@ struct BfsTable {
         const int32_t s = __ldg(&a.row_ptr[v]), e = __ldg(&a.row_ptr[v + 1]);
         const int32_t nd = dv + 1;
         const uint32_t bd = blockDim.x;
-        const uint32_t chunk_every = max(1u, (uint32_t)kSpawnCap / (2u * bd));  // spawns between checks <= chunk_every*bd
+        // kU edges per thread per step: the kU col loads and then the kU atomicMin are independent,
+        // so a hub's expansion keeps kU round trips in flight per thread (data-parallel body)
+        // ue <= kU edges per thread per step, so that one step stages at most half the spawn buffer
+        const uint32_t ue = max(1u, min(kU, (uint32_t)kSpawnCap / (2u * bd)));
+        const uint32_t step = ue * bd;
+        const uint32_t chunk_every = max(1u, (uint32_t)kSpawnCap / (2u * step));  // spawns between checks
         uint32_t k = 0;
-        for (int32_t base = s; base < e; base += (int32_t)bd) {
-            const int32_t i = base + (int32_t)threadIdx.x;
-            if (i < e) {
-                const int32_t u = __ldg(&a.col[i]);
-                const int32_t old = atomicMin(&a.depth[u], nd);
-                if (old > nd) ctx.spawn(0u, (uint32_t)u);
+        for (int32_t base = s; base < e; base += (int32_t)step) {
+            int32_t u[kU];
+#pragma unroll
+            for (int j = 0; j < kU; ++j) {
+                const int32_t i = base + (int32_t)(threadIdx.x + j * bd);
+                u[j] = ((uint32_t)j < ue && i < e) ? __ldg(&a.col[i]) : -1;
             }
+            int32_t old[kU];
+#pragma unroll
+            for (int j = 0; j < kU; ++j) old[j] = u[j] >= 0 ? atomicMin(&a.depth[u[j]], nd) : nd;
+#pragma unroll
+            for (int j = 0; j < kU; ++j)
+                if (old[j] > nd) ctx.spawn(0u, (uint32_t)u[j]);
             if (++k == chunk_every) {                               // uniform
                 k = 0;
-                if (base + (int32_t)bd < e) ctx.flush(chunk_every * bd);
+                if (base + (int32_t)step < e) ctx.flush(chunk_every * step);
             }
         }
         if (threadIdx.x == 0) ctx.finish_void();

@@ -16,6 +16,7 @@
 // root (depth 0) ends in `keys`. The output is the unique sorted permutation
 // either way. Payload: d[0] = l, d[1] = r, d[2] = depth.
 #include <climits>
+#include <type_traits>
 
 #include "table_common.cuh"
 
@@ -205,31 +206,42 @@ struct MergeSlot {                           // placed 2 KB-aligned inside the b
     uint32_t par[2 * kChains];               // mbarrier parity bits per input ring
 };
 // warp-assist merge tiles (GTAP_MERGE_WARP): per warp, one smem ring per input run
-constexpr int kWT = 256;                     // outputs per tile
+#ifndef GTAP_MS_WT
+#define GTAP_MS_WT 256
+#endif
+#ifndef GTAP_MS_WR
+#define GTAP_MS_WR 1024
+#endif
+constexpr int kWT = GTAP_MS_WT;              // outputs per tile
 constexpr int kVT = kWT / 32;                // outputs per lane per tile
-constexpr int kWR = 1024;                    // keys per ring (window + 3 tiles of prefetch)
+constexpr int kWR = GTAP_MS_WR;              // keys per ring
+constexpr uint32_t kTopChunk = kWT / 2;      // cp.async top-up granule
+// window issued >= 2 tiles before it is read (wait_group 1): top-ups trail pa + kWR by < kTopChunk
+// keys and a tile consumes <= kWT keys of a run
+static_assert(kWR >= 3 * kWT + (int)kTopChunk - 1, "ring too small for wait_group 1");
+static_assert((kWR & (kWR - 1)) == 0 && kWT % 64 == 0, "ring: power of two; tile: multiple of 64");
 struct WarpTiles {
     int32_t a[kWR];
     int32_t b[kWR];
 };
 constexpr int kMsWarps = 4;                  // kMaxThreads / 32
-constexpr size_t cmax(size_t x, size_t y) { return x > y ? x : y; }
-struct MergeSlotHolder {                     // BlockExtra: 2 KB of slack to align the slot
-    // the TMA slot (GTAP_MERGE_THREAD) and the warp tiles (GTAP_MERGE_WARP) share the space:
-    // a table uses one or the other
-    unsigned char raw[cmax(sizeof(MergeSlot) + 2048, sizeof(WarpTiles) * kMsWarps + 128)];
+struct MergeSlotHolder {                     // BlockExtra of merge_mode thread: 2 KB of slack to align the slot
+    unsigned char raw[sizeof(MergeSlot) + 2048];
     uint32_t busy;
-    // block assist board (GTAP_MERGE_WARP, merges >= kBlockAssistMin): one open merge per block
+    __device__ __forceinline__ MergeSlot* slot() {
+        const uint32_t a = tma::sa(raw);
+        return reinterpret_cast<MergeSlot*>(raw + ((2048u - (a & 2047u)) & 2047u));
+    }
+};
+struct WarpAssistHolder {                    // BlockExtra of merge_mode warp: per-warp rings + block board
+    unsigned char raw[sizeof(WarpTiles) * kMsWarps + 128];
+    // block assist board (merges >= kBlockAssistMin): one open merge per block
     struct Board {
         uint32_t state;               // 0 free, 1 being set up, 2 open
         uint32_t l, m, r, depth;
         uint32_t next;                // next chunk to claim (>= nchunks: closed)
         uint32_t nchunks, done;
     } board;
-    __device__ __forceinline__ MergeSlot* slot() {
-        const uint32_t a = tma::sa(raw);
-        return reinterpret_cast<MergeSlot*>(raw + ((2048u - (a & 2047u)) & 2047u));
-    }
     __device__ __forceinline__ WarpTiles* tiles(uint32_t warp) {
         const uint32_t a = tma::sa(raw);
         return reinterpret_cast<WarpTiles*>(raw + ((128u - (a & 127u)) & 127u)) + warp;
@@ -597,17 +609,17 @@ __device__ __forceinline__ void cp4(const int32_t* sdst, const int32_t* gsrc) {
 __device__ __forceinline__ void commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-// lanes copy src[from, to) into ring positions (global index & (kWR - 1)): whole 128-key chunks
-// (4 copies per lane, no tail) while they fit, the rest only at the run's end. Returns the new `from`.
+// lanes copy src[from, to) into ring positions (global index & (kWR - 1)): whole kTopChunk-key
+// chunks (no tail) while they fit, the rest only at the run's end. Returns the new `from`.
 __device__ __forceinline__ uint32_t topup(int32_t* ring, const int32_t* src, uint32_t from, uint32_t to,
                                           uint32_t end, uint32_t lane) {
-    while (from + 128u <= to) {
+    while (from + kTopChunk <= to) {
 #pragma unroll
-        for (uint32_t k = 0; k < 4u; ++k) {
+        for (uint32_t k = 0; k < kTopChunk / 32u; ++k) {
             const uint32_t i = from + lane + 32u * k;
             cp4(ring + (i & (kWR - 1u)), src + i);
         }
-        from += 128u;
+        from += kTopChunk;
     }
     if (to == end) {
         for (uint32_t i = from + lane; i < to; i += 32u) cp4(ring + (i & (kWR - 1u)), src + i);
@@ -632,7 +644,7 @@ __device__ __noinline__ void warp_merge(const int32_t* __restrict__ src, int32_t
     wm::commit();
     while (out < oend) {
         const uint32_t tile = min((uint32_t)kWT, oend - out);
-        wm::wait<1>();  // the window was issued >= 2 tiles ago (top-ups trail pa + kWR by < 128 keys)
+        wm::wait<1>();  // the window was issued >= 2 tiles ago (see kTopChunk)
         __syncwarp();
         const uint32_t na = min(tile, m - pa), nb = min(tile, r - pb);
         const uint32_t d = min(lane * (uint32_t)kVT, tile);
@@ -854,6 +866,22 @@ struct GBoard {
     GSlot slot[kGSlots];
 };
 
+#ifndef GTAP_MS_WARP_MINB
+#define GTAP_MS_WARP_MINB 4
+#endif
+
+struct MsArgs {
+    int32_t* keys;
+    int32_t* scratch;
+    uint32_t cutoff;
+    uint32_t n;         // array length (TMA path needs n % 4 == 0 and 16-B aligned buffers)
+    uint32_t mode;      // GTAP_MERGE_THREAD (0) or GTAP_MERGE_WARP (1)
+    uint32_t pad;
+    GBoard* gb;         // GPU-wide assist board (table-owned, reset before each run)
+};
+
+// MODE: GTAP_MERGE_THREAD (0, one-lane bodies, TMA merge slot) or GTAP_MERGE_WARP (1, warp assist)
+template <uint32_t MODE>
 struct MergesortTable {
     static constexpr uint32_t kKind = GTAP_WORKER_THREAD;
     static constexpr int kMaxChildren = 2;
@@ -867,24 +895,17 @@ struct MergesortTable {
     __device__ __forceinline__ static bool heavy_parent(uint32_t, const uint32_t* d) {
         return 2u * (d[1] - d[0]) >= kTmaMin;
     }
-    static constexpr int kMaxThreads = 128, kMinBlocks = 4;  // __launch_bounds__: 128 regs, no spills
-    static constexpr bool kAssist = true;                    // heavy merges: warp assist (merge_mode 1)
+    static constexpr int kMaxThreads = 128;                    // __launch_bounds__
+    static constexpr int kMinBlocks = MODE == 1u ? GTAP_MS_WARP_MINB : 4;
+    static constexpr bool kAssist = MODE == 1u;                // leaf and merge bodies: warp assist
 #ifndef GTAP_MS_ASSIST_MIN
 #define GTAP_MS_ASSIST_MIN 0
 #endif
     static constexpr uint32_t kAssistMin = GTAP_MS_ASSIST_MIN;
-    struct Args {
-        int32_t* keys;
-        int32_t* scratch;
-        uint32_t cutoff;
-        uint32_t n;         // array length (TMA path needs n % 4 == 0 and 16-B aligned buffers)
-        uint32_t mode;      // GTAP_MERGE_THREAD (0) or GTAP_MERGE_WARP (1)
-        uint32_t pad;
-        GBoard* gb;         // GPU-wide assist board (table-owned, reset before each run)
-    };
+    using Args = MsArgs;
     // warp assist: ap = {l, r, depth}; all 32 lanes
     __device__ __forceinline__ static bool assist(const Args& a, const uint32_t (&ap)[kDataWords], uint32_t lane,
-                                                  MergeSlotHolder* H) {
+                                                  WarpAssistHolder* H) {
         static_assert(kMaxThreads / 32 <= kMsWarps, "one WarpTiles per warp");
         const uint32_t l = ap[0], r = ap[1], depth = ap[2];
         MS_T0;
@@ -907,7 +928,7 @@ struct MergesortTable {
         if (r - l >= kBlockAssistMin) {
             // block assist: open the board, merge chunks alongside the block's other warps (they
             // join at the top of their scheduler loops), wait until every chunk is done
-            volatile MergeSlotHolder::Board& B = H->board;
+            volatile WarpAssistHolder::Board& B = H->board;
             uint32_t got = 0;
             if (lane == 0) got = (atomicCAS(&H->board.state, 0u, 1u) == 0u) ? 1u : 0u;
             if (__shfl_sync(0xffffffffu, got, 0)) {
@@ -940,8 +961,8 @@ struct MergesortTable {
     }
 
     // claim and merge chunks of the block's open board until none is left (all 32 lanes)
-    __device__ __noinline__ static void help_chunks(const Args& a, MergeSlotHolder* H, uint32_t lane, WarpTiles* T) {
-        volatile MergeSlotHolder::Board& B = H->board;
+    __device__ __noinline__ static void help_chunks(const Args& a, WarpAssistHolder* H, uint32_t lane, WarpTiles* T) {
+        volatile WarpAssistHolder::Board& B = H->board;
         while (true) {
             uint32_t c = 0;
             if (lane == 0) c = atomicAdd(&H->board.next, 1u);
@@ -1066,29 +1087,32 @@ struct MergesortTable {
     }
 
     // scheduler hook, idle path (all 32 lanes): help an open GPU-wide assist
-    __device__ __forceinline__ static bool help_idle(const Args& a, uint32_t lane, MergeSlotHolder* H) {
+    __device__ __forceinline__ static bool help_idle(const Args& a, uint32_t lane, WarpAssistHolder* H) {
         if (a.gb == nullptr) return false;
         return help_global_once(a, lane, H->tiles(threadIdx.x >> 5));
     }
 
     // scheduler hook, top of every cycle (all 32 lanes): join an open board of this block
-    __device__ __forceinline__ static void help(const Args& a, uint32_t lane, MergeSlotHolder* H) {
+    __device__ __forceinline__ static void help(const Args& a, uint32_t lane, WarpAssistHolder* H) {
         if (reinterpret_cast<volatile uint32_t&>(H->board.state) == 2u)
             help_chunks(a, H, lane, H->tiles(threadIdx.x >> 5));
     }
-    using BlockExtra = MergeSlotHolder;
+    using BlockExtra = std::conditional_t<MODE == 1u, WarpAssistHolder, MergeSlotHolder>;
     __device__ __forceinline__ static void block_init(BlockExtra* H) {
-        MergeSlot* S = H->slot();
-        for (int k = 0; k < 2 * kChains; ++k) {
-            for (int j = 0; j < 2; ++j) tma::mbar_init(&S->mbar[k][j], 1);
-            S->par[k] = 0;
+        if constexpr (MODE == 1u) {
+            H->board.state = 0;
+            H->board.next = 0x80000000u;
+            H->board.nchunks = 0;
+            H->board.done = 0;
+        } else {
+            MergeSlot* S = H->slot();
+            for (int k = 0; k < 2 * kChains; ++k) {
+                for (int j = 0; j < 2; ++j) tma::mbar_init(&S->mbar[k][j], 1);
+                S->par[k] = 0;
+            }
+            H->busy = 0;
+            tma::fence_smem();
         }
-        H->busy = 0;
-        H->board.state = 0;
-        H->board.next = 0x80000000u;
-        H->board.nchunks = 0;
-        H->board.done = 0;
-        tma::fence_smem();
     }
 
     __device__ __forceinline__ static int32_t* buf(const Args& a, uint32_t depth) {
@@ -1140,14 +1164,13 @@ struct MergesortTable {
         switch (state) {
             case 0:
                 if (r - l <= a.cutoff) {
-                    if (a.mode == 1u) {                       // by the whole warp (bitonic, registers)
+                    if constexpr (MODE == 1u) {               // by the whole warp (bitonic, registers)
                         o.request_assist(l, r, depth, 1u);
-                        o.finish_void();
-                        return;
+                    } else {
+                        MS_T0;
+                        leaf_sort(a.keys, buf(a, depth), l, r);
+                        MS_TRACE(r - l, l, 2u);
                     }
-                    MS_T0;
-                    leaf_sort(a.keys, buf(a, depth), l, r);
-                    MS_TRACE(r - l, l, 2u);
                     o.finish_void();
                     return;
                 } else {
@@ -1158,13 +1181,17 @@ struct MergesortTable {
                     return;
                 }
             case 1: {
-                if (a.mode == 1u && r - l >= kAssistMin) {  // merge(l, m, r) by the whole warp
-                    o.request_assist(l, r, depth, 0u);
-                    o.finish_void();
-                    return;
-                }
                 const uint32_t m = l + (r - l) / 2u;
-                if (!merge(a, buf(a, depth + 1u), buf(a, depth), l, m, r, S)) { o.bad_state(); return; }
+                if constexpr (MODE == 1u) {
+                    if (r - l >= kAssistMin) {                // merge(l, m, r) by the whole warp
+                        o.request_assist(l, r, depth, 0u);
+                        o.finish_void();
+                        return;
+                    }
+                    ms_merge(buf(a, depth + 1u), buf(a, depth), l, m, r);
+                } else {
+                    if (!merge(a, buf(a, depth + 1u), buf(a, depth), l, m, r, S)) { o.bad_state(); return; }
+                }
                 o.finish_void();
                 return;
             }
@@ -1187,8 +1214,10 @@ extern "C" const gtap_task_table* gtap_table_mergesort_ex(int32_t* keys, int32_t
     if (merge_mode > 1u) return nullptr;
     gtap::GBoard* gb = nullptr;
     if (merge_mode == 1u && cudaMalloc(&gb, sizeof(gtap::GBoard)) != cudaSuccess) return nullptr;
-    gtap::MergesortTable::Args a{keys, scratch, (uint32_t)cutoff, (uint32_t)n, merge_mode, 0u, gb};
-    gtap_task_table* t = gtap::make_table<gtap::MergesortTable>("mergesort", a, &gtap::validate_ms);
+    gtap::MsArgs a{keys, scratch, (uint32_t)cutoff, (uint32_t)n, merge_mode, 0u, gb};
+    gtap_task_table* t = merge_mode == 1u
+        ? gtap::make_table<gtap::MergesortTable<1u>>("mergesort_warp", a, &gtap::validate_ms)
+        : gtap::make_table<gtap::MergesortTable<0u>>("mergesort", a, &gtap::validate_ms);
     if (!t) { cudaFree(gb); return nullptr; }
     if (gb) {
         t->dev_scratch = gb;

@@ -472,8 +472,13 @@ def cpu_baseline(sample_n=1 << 22, budget_s=12.0):
         oracle.mergesort(keys, MS_CUTOFF)
         t_tot += time.perf_counter() - t0
         reps += 1
+    # context for the paper's only fib ratio (GPU 2.4x faster than one CPU core at fib(40))
+    t0 = time.perf_counter()
+    oracle.fib(FIB_N)
+    fib_s = time.perf_counter() - t0
     return dict(value=sample_n * reps / t_tot / 1e6, unit=UNIT, cores=1, kind="oracle",
-                sample=f"{reps} x oracle mergesort of 2^{sample_n.bit_length() - 1} seeded int32 keys, cutoff 128")
+                sample=f"{reps} x oracle mergesort of 2^{sample_n.bit_length() - 1} seeded int32 keys, cutoff 128",
+                fib40_oracle_ms=fib_s * 1e3)
 
 
 def run_ours(args):
@@ -541,6 +546,13 @@ def run_ours(args):
         }
         if ws == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline()
+            for s in line.get("secondary", []):
+                if s.get("workload", "").startswith("fib(40) no cutoff") and "ms" in s:
+                    s["speedup_vs_cpu_oracle"] = line["cpu_baseline"]["fib40_oracle_ms"] / s["ms"]
+                    s["paper_speedup_vs_cpu_seq"] = "2.4x on GH200 vs one Grace core (P:585); context only"
+                if s.get("workload", "").startswith("mergesort 2^24 cutoff 128, merge_mode=thread") and "value" in s:
+                    s["speedup_vs_cpu_oracle"] = s["value"] / line["cpu_baseline"]["value"]
+                    s["paper_note"] = "paper: up to 103x slower than 72-core OpenMP at n = 1e7 (P:592); context only"
         print(json.dumps(line), flush=True)
     if ws > 1:
         import torch.distributed as dist

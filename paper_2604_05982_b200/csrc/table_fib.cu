@@ -18,7 +18,10 @@ struct FibTable {
     static constexpr bool kHasHeavy = false;
     static constexpr uint32_t kNumFn = 1;
     static constexpr bool kJoinReduceAdd = true;  // see TaskRec
-    static constexpr int kMaxThreads = 256, kMinBlocks = 4;  // __launch_bounds__
+#ifndef GTAP_FIB_MINB
+#define GTAP_FIB_MINB 3  // 72 regs, no spills (4: 64 regs + spills, 2% slower)
+#endif
+    static constexpr int kMaxThreads = 256, kMinBlocks = GTAP_FIB_MINB;  // __launch_bounds__
     struct Args {
         uint32_t unused;
     };

@@ -139,3 +139,36 @@ def test_forest_tma_segments(g, mode):
     out = d.cpu().numpy()
     for l, r in segs:
         assert np.array_equal(out[l:r], np.sort(keys[l:r]))
+
+
+@pytest.mark.parametrize("nseg,seg", [(2048, 1 << 15), (600, 1 << 16), (3000, 20011)])
+def test_assist_board_saturation(g, nseg, seg):
+    """merge_mode warp, many concurrent roots: more simultaneous merges >= 2^14 keys than GPU-wide
+    board slots (1024), so requesters fall back to the block board or their own warp while slots
+    open and close under them; every segment must come out sorted and the task counts exact."""
+    import torch
+    keys = synth.keys_int32(nseg * seg, seed=nseg).numpy()
+    d = torch.from_numpy(keys).cuda()
+    segs = [(i * seg, (i + 1) * seg) for i in range(nseg)]
+    st = g.mergesort_forest_(d, segs, merge_mode=1, grid_size=0, block_size=128, max_tasks_per_worker=1024,
+                             idle_backoff_ns=1024, watchdog_ns=WD)
+    out = d.cpu().numpy().reshape(nseg, seg)
+    assert np.array_equal(out, np.sort(keys.reshape(nseg, seg), axis=1))
+    _, tasks, inv = oracle.mergesort(keys[:seg], 128)
+    assert (st.tasks, st.invocations) == (nseg * tasks, nseg * inv)
+
+
+@pytest.mark.parametrize("grid,block", [(1, 32), (3, 128), (148, 64)])
+def test_warp_mode_small_grids(g, grid, block):
+    """merge_mode warp with one warp / few blocks: the block and GPU-wide assists degenerate to the
+    requester doing every chunk itself."""
+    import torch
+    n = (1 << 18) + 77
+    keys = synth.keys_int32(n, seed=5).numpy()
+    d = torch.from_numpy(keys).cuda()
+    with g.Runtime(g.GTAP_WORKER_THREAD, 0, grid_size=grid, block_size=block, max_tasks_per_worker=4096,
+                   watchdog_ns=WD) as r:
+        st = g.mergesort_(d, cutoff=128, merge_mode=1, rt=r)
+    ref, tasks, inv = oracle.mergesort(keys, 128)
+    assert np.array_equal(d.cpu().numpy(), ref)
+    assert (st.tasks, st.invocations) == (tasks, inv)

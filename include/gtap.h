@@ -77,7 +77,8 @@ typedef struct {
     uint32_t assume_no_taskwait;   /* GTAP_ASSUME_NO_TASKWAIT; informative:
                                       tables that never join set it themselves */
     uint32_t steal_attempts;       /* victims probed per idle cycle; 0 = 4 */
-    uint32_t steal_max;            /* max tasks per steal; 0 = 32 (warp) / 1 (block) */
+    uint32_t steal_max;            /* max tasks per steal, <= 32; 0 = 32 (warp) / 1 (block). A block-level
+                                      steal of c > 1 runs one task and keeps c - 1 in the thief's own deque */
     uint32_t max_roots;            /* forest capacity (roots per run); 0 = 65536 */
     uint64_t seed;                 /* victim-selection PRNG seed */
     uint64_t watchdog_ns;          /* 0 = off; else a run longer than this fails with GTAP_E_TIMEOUT */

@@ -70,7 +70,7 @@ gtap_status resolve(const gtap_config* in, gtap_config* c, int sm_count) {
     if (c->steal_attempts == 0) c->steal_attempts = 4;
     if (c->steal_max == 0) c->steal_max = (c->worker_kind == GTAP_WORKER_THREAD) ? 32 : 1;
     if (c->worker_kind == GTAP_WORKER_THREAD && c->steal_max > 32) return GTAP_E_INVAL;
-    if (c->worker_kind == GTAP_WORKER_BLOCK && c->steal_max != 1) return GTAP_E_INVAL;
+    if (c->worker_kind == GTAP_WORKER_BLOCK && c->steal_max > 32) return GTAP_E_INVAL;  // default 1
     if (c->max_roots == 0) c->max_roots = 65536;
     if (c->idle_backoff_ns == 0) c->idle_backoff_ns = 8192;
     if (c->idle_backoff_ns < 32 || c->idle_backoff_ns > 1000000) return GTAP_E_INVAL;

@@ -317,22 +317,41 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) block_sched_ker
                     if ((best >> 5) == 0) { if (lane == 0) ++L.st[ST_STEALS_FAILED]; continue; }
                     const uint32_t victim = __shfl_sync(0xffffffffu, v, best & 31u);
                     DequeMeta* vdq = p.dq + victim;
-                    uint32_t sid = kNone;
+                    // claim c tasks from the head: 1 or, with steal_max > 1, up to half of a
+                    // public part of >= 2 (the thief runs one and keeps c - 1 in its own deque)
+                    uint32_t got = 0, h0 = 0;
                     if (lane == 0 && atom_cas_relaxed(&vdq->lock, 0u, 1u) == 0u) {
                         unsigned long long s = ld_relaxed(&vdq->S);
+                        const uint32_t room = Q - (L.tail - L.sdone);  // own ring space for the extras
                         for (int it = 0; it < 8; ++it) {
                             const uint32_t h = (uint32_t)s, sp = (uint32_t)(s >> 32);
-                            if (sp == h || sp - h > Q) break;
-                            const unsigned long long nw = ((unsigned long long)sp << 32) | (uint32_t)(h + 1u);
+                            const uint32_t avail = sp - h;
+                            if (avail == 0u || avail > Q) break;
+                            const uint32_t c = min(max(1u, min(p.steal_max, avail >> 1)), room + 1u);
+                            const unsigned long long nw = ((unsigned long long)sp << 32) | (uint32_t)(h + c);
                             const unsigned long long o = atom_cas_acquire(&vdq->S, s, nw);
-                            if (o == s) { sid = ld_relaxed(&p.ring[(size_t)victim * Q + (h & qmask)]); break; }
+                            if (o == s) { got = c; h0 = h; break; }
                             s = o;
                         }
-                        if (sid != kNone) red_add_release(&vdq->steal_done, 1u);
-                        st_relaxed(&vdq->lock, 0u);
+                        if (got == 0u) st_relaxed(&vdq->lock, 0u);
                     }
-                    id = __shfl_sync(0xffffffffu, sid, 0);
-                    if (lane == 0) { if (id != kNone) { ++L.st[ST_STEALS_OK]; ++L.st[ST_STOLEN]; } else ++L.st[ST_STEALS_FAILED]; }
+                    got = __shfl_sync(0xffffffffu, got, 0);
+                    uint32_t sidl = kNone;
+                    if (got) {
+                        h0 = __shfl_sync(0xffffffffu, h0, 0);
+                        if (lane < got) sidl = ld_relaxed(&p.ring[(size_t)victim * Q + ((h0 + lane) & qmask)]);
+                        __syncwarp();
+                        if (lane == 0) {  // advance the read prefix only after loading the IDs
+                            red_add_release(&vdq->steal_done, got);
+                            st_relaxed(&vdq->lock, 0u);
+                        }
+                        if (got > 1u) {  // extras onto the own private part
+                            if (lane >= 1u && lane < got) ring[(L.tail + lane - 1u) & qmask] = sidl;
+                            L.tail += got - 1u;
+                        }
+                    }
+                    id = __shfl_sync(0xffffffffu, sidl, 0);
+                    if (lane == 0) { if (id != kNone) { ++L.st[ST_STEALS_OK]; L.st[ST_STOLEN] += got; } else ++L.st[ST_STEALS_FAILED]; }
                 }
             }
             if (id != kNone) {

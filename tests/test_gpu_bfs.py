@@ -105,3 +105,13 @@ def test_full_size_config4(g):
         depth, st = g.bfs(rp, col, src, rt=r)
     ref = oracle.bfs(rp.cpu(), col.cpu(), src)
     assert np.array_equal(depth.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("steal_max", [2, 7, 32])
+def test_batch_steal(g, steal_max):
+    """Block-level batch steals (steal_max > 1: run one, keep the rest): levels stay exact."""
+    rp, col = synth.rmat_csr(14, 16, seed=21)
+    with g.Runtime(g.GTAP_WORKER_BLOCK, 0, grid_size=148 * 4, block_size=64, max_tasks_per_worker=1 << 15,
+                   steal_max=steal_max, watchdog_ns=WD) as r:
+        for s in synth.bfs_sources(rp, 3, seed=steal_max):
+            check(g, r, rp, col, s)

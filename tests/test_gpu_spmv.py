@@ -134,3 +134,11 @@ def test_forest_subrange(g):
     rel = np.abs(y[lo:hi][ne] - y64[lo:hi][ne]) / np.abs(y64[lo:hi][ne])
     assert rel.max() <= RTOL
     assert np.all(y[lo:hi][~ne] == 0.0)
+
+
+@pytest.mark.parametrize("steal_max", [3, 32])
+def test_batch_steal(g, steal_max):
+    rp, col, val, x = synth.powerlaw_csr(20011, seed=13)
+    with g.Runtime(g.GTAP_WORKER_BLOCK, 0, grid_size=148 * 2, block_size=128, max_tasks_per_worker=4096,
+                   steal_max=steal_max, watchdog_ns=WD) as r:
+        check(g, r, rp, col, val, x, nnz_cut=256, fanout=8)

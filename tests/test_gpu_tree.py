@@ -114,3 +114,14 @@ def test_bad_args(g, buf):
     assert not L.gtap_table_tree(g.GTAP_WORKER_BLOCK, 5, 9, 1, buf.data_ptr(), 1024, 1, 1, tot.data_ptr())
     assert not L.gtap_table_tree(g.GTAP_WORKER_BLOCK, 0, 3, 1, buf.data_ptr(), 1024, 1, 1, tot.data_ptr())
     assert not L.gtap_table_tree(7, 5, 0, 1, buf.data_ptr(), 1024, 1, 1, tot.data_ptr())
+
+
+@pytest.mark.parametrize("steal_max", [4, 32])
+def test_block_batch_steal(g, buf, buf_cpu, steal_max):
+    """Block-level batch steals with taskwait (joins of stolen children land in other blocks)."""
+    with g.Runtime(g.GTAP_WORKER_BLOCK, 0, grid_size=148 * 8, block_size=64, max_tasks_per_worker=2048,
+                   steal_max=steal_max, watchdog_ns=WD) as r:
+        total, st = g.tree(14, buf, 5, 70, worker=g.GTAP_WORKER_BLOCK, rt=r)
+        assert (total, st.tasks) == oracle.tree(14, _np(buf_cpu), 5, 70)
+        total, st = g.tree(16, buf, 5, 70, pruned=True, seed=9, worker=g.GTAP_WORKER_BLOCK, rt=r)
+        assert (total, st.tasks) == oracle.tree(16, _np(buf_cpu), 5, 70, pruned=True, seed=9)

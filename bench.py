@@ -51,7 +51,7 @@ NQ_N = 16
 NQ_CUTOFF = 7
 NQ_CFG = dict(grid_size=0, block_size=128, max_tasks_per_worker=4096)
 BFS_SCALE = 22
-BFS_CFG = dict(grid_size=148 * 16, block_size=64, max_tasks_per_worker=1 << 17, idle_backoff_ns=1024,
+BFS_CFG = dict(grid_size=148 * 16, block_size=64, max_tasks_per_worker=1 << 18, idle_backoff_ns=1024,
                steal_max=32)  # batch steals (the paper's block-level steal takes 1): 33 -> 8.6 ms
 
 L2_FLUSH_BYTES = 256 << 20

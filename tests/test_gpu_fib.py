@@ -42,7 +42,7 @@ def test_fib20_config0(g, rt):
     assert (v, st.tasks, st.invocations) == (6765, 21891, 32836)  # BASELINE configs[0]
 
 
-@pytest.mark.parametrize("grid,block", [(1, 32), (1, 128), (2, 32), (7, 64), (148, 32), (148 * 8, 128), (0, 256)])
+@pytest.mark.parametrize("grid,block", [(1, 32), (1, 128), (2, 32), (7, 64), (148, 32), (148 * 7, 128), (0, 256)])
 def test_fib_geometry(g, grid, block):
     with g.Runtime(g.GTAP_WORKER_THREAD, 0, grid_size=grid, block_size=block, max_tasks_per_worker=2048,
                    watchdog_ns=WD) as r:

@@ -46,7 +46,7 @@ SPMV_NNZ_CUT = 8192
 SPMV_FANOUT = 32
 SPMV_PARTS = 148 * 8     # forest: one nnz-balanced root per worker (fn part(k, R), reading R20)
 SPMV_CFG = dict(grid_size=148 * 8, block_size=128, max_tasks_per_worker=1024, max_roots=SPMV_PARTS)
-CS_CFG = dict(grid_size=0, block_size=128, max_tasks_per_worker=4096)
+CS_CFG = dict(grid_size=0, block_size=128, max_tasks_per_worker=4096, idle_backoff_ns=1024)
 NQ_N = 16
 NQ_CUTOFF = 7
 NQ_CFG = dict(grid_size=0, block_size=128, max_tasks_per_worker=4096)

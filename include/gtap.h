@@ -233,6 +233,11 @@ const gtap_task_table *gtap_table_mergesort_ex(int32_t *keys, int32_t *scratch, 
  * 256). Output sorted in keys. fn 0, root args {uint32 l, uint32 r}. */
 const gtap_task_table *gtap_table_cilksort(int32_t *keys, int32_t *scratch, uint64_t n, int32_t cut_sort,
                                            int32_t cut_merge);
+/* Cilksort with an explicit merge_mode (GTAP_MERGE_THREAD: leaf sorts and sequential merges on
+ * the task's lane; GTAP_MERGE_WARP: those bodies run by the task's warp -- bitonic networks, same
+ * task graph and output). gtap_table_cilksort is merge_mode GTAP_MERGE_WARP. */
+const gtap_task_table *gtap_table_cilksort_ex(int32_t *keys, int32_t *scratch, uint64_t n, int32_t cut_sort,
+                                              int32_t cut_merge, uint32_t merge_mode);
 
 /* SpMV y = A x over CSR (P:42 names SpMV as block-cooperative), block-level,
  * no taskwait. Task spmv(lo, hi) splits the row range into `fanout` equal

@@ -118,14 +118,15 @@ def mergesort_(keys, scratch=None, cutoff: int = 128, merge_mode: int = 1, rt: R
             rt.close()
 
 
-def cilksort_(keys, scratch=None, cut_sort: int = 64, cut_merge: int = 256, rt: Runtime | None = None, stream=None,
+def cilksort_(keys, scratch=None, cut_sort: int = 64, cut_merge: int = 256, merge_mode: int = 1,
+              rt: Runtime | None = None, stream=None,
               **cfg):
     """Sort a CUDA int32 tensor in place with Cilksort (parallel merge)."""
     import torch
     if scratch is None:
         scratch = torch.empty_like(keys)
     rt, own = _runtime(GTAP_WORKER_THREAD, rt, keys.device.index or 0, cfg)
-    table = Table.cilksort(keys, scratch, cut_sort, cut_merge)
+    table = Table.cilksort(keys, scratch, cut_sort, cut_merge, merge_mode)
     try:
         rt.spawn_root(table, (0, keys.numel()))
         rt.run(stream)

@@ -15,6 +15,7 @@
 // oracle (reading R26). The merge payload packs a0, a1, b0, b1, m (25 bits
 // each) and the destination parity into the 16-B record payload: n < 2^25.
 #include "table_common.cuh"
+#include "warp_sort.cuh"
 
 namespace gtap {
 
@@ -65,19 +66,27 @@ __device__ __noinline__ void cs_seq_merge(const int32_t* __restrict__ a, uint32_
     while (j < nb) out[k++] = b[j++];
 }
 
+struct CsArgs {
+    int32_t* keys;
+    int32_t* scratch;
+    uint32_t cut_sort, cut_merge;
+    uint32_t mode, pad;
+};
+
+// MODE: GTAP_MERGE_THREAD (0: leaf sorts and sequential merges on the task's lane) or
+// GTAP_MERGE_WARP (1: those bodies run by the task's warp, R28; same task graph)
+template <uint32_t MODE>
 struct CilksortTable {
     static constexpr uint32_t kKind = GTAP_WORKER_THREAD;
+    static constexpr bool kAssist = MODE == 1u;
+    static constexpr uint32_t kMergeBit = 0x80000000u;  // ap[3] bit 31 (free in the packed descriptor)
     static constexpr int kMaxChildren = 2;
     static constexpr bool kTaskwait = true;
     static constexpr bool kHasHeavy = false;
     static constexpr uint32_t kNumFn = 2;
     static constexpr bool kJoinReduceAdd = false;
     static constexpr int kMaxThreads = 256, kMinBlocks = 2;  // __launch_bounds__
-    struct Args {
-        int32_t* keys;
-        int32_t* scratch;
-        uint32_t cut_sort, cut_merge;
-    };
+    using Args = CsArgs;
     struct BlockExtra {
         uint32_t unused;
     };
@@ -85,6 +94,27 @@ struct CilksortTable {
     __device__ __forceinline__ static int32_t* buf(const Args& a, uint32_t parity) {
         return parity ? a.scratch : a.keys;
     }
+
+    // warp assist (all 32 lanes): ap = {l, r, parity, 0} for a leaf sort, the packed merge
+    // descriptor with kMergeBit for a sequential merge
+    __device__ __forceinline__ static bool assist(const Args& a, const uint32_t (&ap)[kDataWords], uint32_t lane,
+                                                  BlockExtra*) {
+        if (ap[3] & kMergeBit) {
+            const uint32_t md[kDataWords] = {ap[0], ap[1], ap[2], ap[3] & ~kMergeBit};
+            const MergeDesc x = unpack_merge(md);
+            const int32_t* src = buf(a, x.p ^ 1u);
+            int32_t* out = buf(a, x.p) + (x.a0 + x.b0 - x.m);
+            const uint32_t na = x.a1 - x.a0, nb = x.b1 - x.b0;
+            if (na + nb <= kBitonicMax) warp_merge_small(src + x.a0, na, src + x.b0, nb, out, lane);
+            else if (lane == 0) cs_seq_merge(src + x.a0, na, src + x.b0, nb, out);
+            return true;
+        }
+        warp_leaf_sort(a.keys, buf(a, ap[2]), ap[0], ap[1], lane);
+        return true;
+    }
+    // no shared assist boards: the scheduler's help hooks are no-ops
+    __device__ __forceinline__ static void help(const Args&, uint32_t, BlockExtra*) {}
+    __device__ __forceinline__ static bool help_idle(const Args&, uint32_t, BlockExtra*) { return false; }
 
     __device__ __forceinline__ static void exec(const Args& a, uint32_t fn, uint32_t state,
                                                 const uint32_t (&d)[kDataWords], TOut<kMaxChildren>& o,
@@ -95,7 +125,8 @@ struct CilksortTable {
             switch (state) {
                 case 0:
                     if (r - l <= a.cut_sort) {
-                        cs_leaf_sort(a.keys, buf(a, depth & 1u), l, r);
+                        if constexpr (MODE == 1u) o.request_assist(l, r, depth & 1u, 0u);
+                        else cs_leaf_sort(a.keys, buf(a, depth & 1u), l, r);
                         o.finish_void();
                     } else {
                         o.spawn(0, 0u, l, m, depth + 1u);
@@ -126,7 +157,8 @@ struct CilksortTable {
             int32_t* dst = buf(a, x.p);
             const uint32_t na = x.a1 - x.a0, nb = x.b1 - x.b0;
             if (na + nb <= a.cut_merge) {
-                cs_seq_merge(src + x.a0, na, src + x.b0, nb, dst + (x.a0 + x.b0 - x.m));
+                if constexpr (MODE == 1u) o.request_assist(d[0], d[1], d[2], d[3] | kMergeBit);
+                else cs_seq_merge(src + x.a0, na, src + x.b0, nb, dst + (x.a0 + x.b0 - x.m));
                 o.finish_void();
                 return;
             }
@@ -164,11 +196,17 @@ static int validate_cs(const gtap_task_table*, uint32_t fn, const uint32_t* d) {
 
 // Cilksort: keys/scratch int32[n] device buffers, n < 2^25; cut_sort in [1, 256],
 // cut_merge >= 2 (paper: 64 / 256). fn 0 = sort, root args {uint32 l, uint32 r} (normally {0, n}).
+extern "C" const gtap_task_table* gtap_table_cilksort_ex(int32_t* keys, int32_t* scratch, uint64_t n,
+                                                         int32_t cut_sort, int32_t cut_merge, uint32_t merge_mode) {
+    if (((!keys || !scratch) && n > 0) || n >= (1ull << 25) || cut_sort < 1 ||
+        cut_sort > (int32_t)gtap::kCsMaxSortCut || cut_merge < 2 || merge_mode > 1u)
+        return nullptr;
+    gtap::CsArgs a{keys, scratch, (uint32_t)cut_sort, (uint32_t)cut_merge, merge_mode, 0u};
+    return merge_mode == 1u ? gtap::make_table<gtap::CilksortTable<1u>>("cilksort_warp", a, &gtap::validate_cs)
+                            : gtap::make_table<gtap::CilksortTable<0u>>("cilksort", a, &gtap::validate_cs);
+}
+
 extern "C" const gtap_task_table* gtap_table_cilksort(int32_t* keys, int32_t* scratch, uint64_t n, int32_t cut_sort,
                                                       int32_t cut_merge) {
-    if (((!keys || !scratch) && n > 0) || n >= (1ull << 25) || cut_sort < 1 ||
-        cut_sort > (int32_t)gtap::kCsMaxSortCut || cut_merge < 2)
-        return nullptr;
-    gtap::CilksortTable::Args a{keys, scratch, (uint32_t)cut_sort, (uint32_t)cut_merge};
-    return gtap::make_table<gtap::CilksortTable>("cilksort", a, &gtap::validate_cs);
+    return gtap_table_cilksort_ex(keys, scratch, n, cut_sort, cut_merge, 1u);
 }

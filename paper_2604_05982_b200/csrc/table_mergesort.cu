@@ -19,6 +19,7 @@
 #include <type_traits>
 
 #include "table_common.cuh"
+#include "warp_sort.cuh"
 
 namespace gtap {
 
@@ -689,124 +690,6 @@ __device__ __noinline__ void warp_merge(const int32_t* __restrict__ src, int32_t
     __syncwarp();
 }
 
-// all 32 lanes: sort the x[k] (element k * 32 + lane) ascending by a bitonic network (shuffles
-// for partners in other lanes, register compare-exchange for partners in the same lane)
-template <int K>
-__device__ __forceinline__ void warp_bitonic(int32_t (&x)[K], uint32_t lane) {
-    constexpr int N = 32 * K;
-#pragma unroll
-    for (int size = 2; size <= N; size <<= 1) {
-#pragma unroll
-        for (int stride = size >> 1; stride > 0; stride >>= 1) {
-            if (stride >= 32) {
-#pragma unroll
-                for (int k = 0; k < K; ++k) {
-                    const int kk = k ^ (stride >> 5);
-                    if (kk > k) {
-                        const bool up = (((uint32_t)k * 32u + lane) & (uint32_t)size) == 0u;
-                        const int32_t a = x[k], b = x[kk];
-                        const bool sw = up ? (a > b) : (a < b);
-                        x[k] = sw ? b : a;
-                        x[kk] = sw ? a : b;
-                    }
-                }
-            } else {
-#pragma unroll
-                for (int k = 0; k < K; ++k) {
-                    const int32_t p = __shfl_xor_sync(0xffffffffu, x[k], stride);
-                    const bool up = (((uint32_t)k * 32u + lane) & (uint32_t)size) == 0u;
-                    const bool lower = (lane & (uint32_t)stride) == 0u;
-                    x[k] = (lower == up) ? min(x[k], p) : max(x[k], p);
-                }
-            }
-        }
-    }
-}
-
-// all 32 lanes: src[l, r) sorted into dst[l, r) (r - l <= 32 K), padded with INT32_MAX
-template <int K>
-__device__ __noinline__ void warp_leaf_sort_k(const int32_t* __restrict__ src, int32_t* __restrict__ dst, uint32_t l,
-                                              uint32_t r, uint32_t lane) {
-    const uint32_t n = r - l;
-    int32_t x[K];
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-        const uint32_t i = (uint32_t)k * 32u + lane;
-        x[k] = i < n ? src[l + i] : INT_MAX;
-    }
-    warp_bitonic<K>(x, lane);
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-        const uint32_t i = (uint32_t)k * 32u + lane;
-        if (i < n) dst[l + i] = x[k];
-    }
-}
-
-// all 32 lanes: merge of src[l, m) and src[m, r) (r - l <= 32 K) by one bitonic merge network:
-// A ascending, INT32_MAX padding, B reversed is a bitonic sequence of 32 K keys; log2(32 K) half-cleaner
-// stages sort it ascending and the first r - l keys are the merge (integer keys: equal keys are
-// indistinguishable, so the result is the stable merge's)
-template <int K>
-__device__ __noinline__ void warp_merge_bitonic_k(const int32_t* __restrict__ src, int32_t* __restrict__ dst,
-                                                  uint32_t l, uint32_t m, uint32_t r, uint32_t lane) {
-    constexpr uint32_t N = 32u * K;
-    const uint32_t na = m - l, nb = r - m;
-    int32_t x[K];
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-        const uint32_t i = (uint32_t)k * 32u + lane;
-        x[k] = i < na ? src[l + i] : (i >= N - nb ? src[m + (N - 1u - i)] : INT_MAX);
-    }
-#pragma unroll
-    for (uint32_t stride = N >> 1; stride > 0; stride >>= 1) {
-        if (stride >= 32u) {
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-                const int kk = k ^ (int)(stride >> 5);
-                if (kk > k) {
-                    const int32_t a = x[k], b = x[kk];
-                    x[k] = min(a, b);
-                    x[kk] = max(a, b);
-                }
-            }
-        } else {
-            const bool lower = (lane & stride) == 0u;
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-                const int32_t p = __shfl_xor_sync(0xffffffffu, x[k], stride);
-                x[k] = lower ? min(x[k], p) : max(x[k], p);
-            }
-        }
-    }
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-        const uint32_t i = (uint32_t)k * 32u + lane;
-        if (i < r - l) dst[l + i] = x[k];
-    }
-}
-
-constexpr uint32_t kBitonicMax = 1024;  // merges up to this many keys: one bitonic network
-
-__device__ __forceinline__ void warp_merge_small(const int32_t* src, int32_t* dst, uint32_t l, uint32_t m, uint32_t r,
-                                                 uint32_t lane) {
-    const uint32_t n = r - l;
-    if (n <= 32u) warp_merge_bitonic_k<1>(src, dst, l, m, r, lane);
-    else if (n <= 64u) warp_merge_bitonic_k<2>(src, dst, l, m, r, lane);
-    else if (n <= 128u) warp_merge_bitonic_k<4>(src, dst, l, m, r, lane);
-    else if (n <= 256u) warp_merge_bitonic_k<8>(src, dst, l, m, r, lane);
-    else if (n <= 512u) warp_merge_bitonic_k<16>(src, dst, l, m, r, lane);
-    else warp_merge_bitonic_k<32>(src, dst, l, m, r, lane);
-}
-
-__device__ __forceinline__ void warp_leaf_sort(const int32_t* src, int32_t* dst, uint32_t l, uint32_t r,
-                                               uint32_t lane) {
-    const uint32_t n = r - l;
-    if (n <= 32u) warp_leaf_sort_k<1>(src, dst, l, r, lane);
-    else if (n <= 64u) warp_leaf_sort_k<2>(src, dst, l, r, lane);
-    else if (n <= 128u) warp_leaf_sort_k<4>(src, dst, l, r, lane);
-    else warp_leaf_sort_k<8>(src, dst, l, r, lane);
-}
-
 // all 32 lanes: stable merge-path splits (A keys among the first t outputs of merge(src[l, m), src[m, r)))
 // over global memory, 32 probes per step (a ~33-way search: ~5 dependent round trips for 2^23 keys);
 // both splits of a chunk [t0, t1) in lockstep (one dependent round trip per step for the pair)
@@ -916,7 +799,8 @@ struct MergesortTable {
         }
         const uint32_t m = l + (r - l) / 2u;
         if (r - l <= kBitonicMax) {
-            warp_merge_small(buf(a, depth + 1u), buf(a, depth), l, m, r, lane);
+            const int32_t* src = buf(a, depth + 1u);
+            warp_merge_small(src + l, m - l, src + m, r - m, buf(a, depth) + l, lane);
             MS_TRACE_LANE0(r - l, l, 3u);
             return true;
         }

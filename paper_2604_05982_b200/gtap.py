@@ -62,7 +62,7 @@ class Stats(ctypes.Structure):
 EXPORTS = [
     "gtap_abi_version", "gtap_status_str", "gtap_config_default", "gtap_workspace_bytes", "gtap_init",
     "gtap_spawn_root", "gtap_reset", "gtap_run", "gtap_sync", "gtap_root_result", "gtap_finalize",
-    "gtap_geometry", "gtap_table_destroy", "gtap_table_fib", "gtap_table_fib_cutoff", "gtap_table_nqueens", "gtap_table_tree", "gtap_table_mergesort", "gtap_table_mergesort_ex", "gtap_table_cilksort",
+    "gtap_geometry", "gtap_table_destroy", "gtap_table_fib", "gtap_table_fib_cutoff", "gtap_table_nqueens", "gtap_table_tree", "gtap_table_mergesort", "gtap_table_mergesort_ex", "gtap_table_cilksort", "gtap_table_cilksort_ex",
     "gtap_table_spmv",
     "gtap_table_bfs", "gtap_bfs_init_depth", "gtap_ubench_atomics",
 ]
@@ -111,6 +111,8 @@ def lib():
     L.gtap_table_mergesort_ex.restype = vp
     L.gtap_table_cilksort.argtypes = [vp, vp, u64, i32, i32]
     L.gtap_table_cilksort.restype = vp
+    L.gtap_table_cilksort_ex.argtypes = [vp, vp, u64, i32, i32, ctypes.c_uint32]
+    L.gtap_table_cilksort_ex.restype = vp
     L.gtap_table_spmv.argtypes = [vp, vp, vp, vp, vp, u32, u32, u32]
     L.gtap_table_spmv.restype = vp
     L.gtap_table_bfs.argtypes = [vp, vp, vp, u32]
@@ -201,9 +203,10 @@ class Table:
                      "mergesort", GTAP_WORKER_THREAD, (keys, scratch))
 
     @staticmethod
-    def cilksort(keys, scratch, cut_sort: int = 64, cut_merge: int = 256) -> "Table":
+    def cilksort(keys, scratch, cut_sort: int = 64, cut_merge: int = 256, merge_mode: int = 1) -> "Table":
         _dev_i32(keys, "keys"); _dev_i32(scratch, "scratch")
-        return Table(lib().gtap_table_cilksort(keys.data_ptr(), scratch.data_ptr(), keys.numel(), cut_sort, cut_merge),
+        return Table(lib().gtap_table_cilksort_ex(keys.data_ptr(), scratch.data_ptr(), keys.numel(), cut_sort, cut_merge,
+                                                  merge_mode),
                      "cilksort", GTAP_WORKER_THREAD, (keys, scratch))
 
     @staticmethod

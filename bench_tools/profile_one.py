@@ -33,6 +33,12 @@ elif wl == "spmv":
         for i in range(reps):
             y, st = g.spmv(rp, col, val, x, nnz_cut=cut, fanout=bench.SPMV_FANOUT, parts=parts, rt=rt)
             print("spmv", rows, st.device_ms, st.tasks, flush=True)
+elif wl == "nq":
+    n = size or 14
+    with g.Runtime(g.GTAP_WORKER_THREAD, 0, **bench.NQ_CFG) as rt:
+        for i in range(reps):
+            c, st = g.nqueens(n, bench.NQ_CUTOFF, rt=rt)
+            print("nq", n, c, st.device_ms, st.tasks, flush=True)
 elif wl == "bfs":
     scale = size or 22
     rp, col = synth.rmat_csr(scale, 16, seed=3, device="cuda")

@@ -189,6 +189,11 @@ const gtap_task_table *gtap_table_fib_cutoff(int32_t cutoff, uint32_t num_queues
  * n in [1, 20]; d_count: caller-owned device uint64, zeroed by the caller,
  * receives the number of solutions. fn 0, root args {} (nbytes 0). */
 const gtap_task_table *gtap_table_nqueens(int32_t n, int32_t cutoff, unsigned long long *d_count);
+/* N-Queens with an explicit leaf_mode: 0 = the paper's serial leaf on the task's lane; 1 = the
+ * task's warp counts the leaf (two rows expanded, sub-problems counted round robin by the lanes;
+ * DESIGN.md R28). Same tasks and count. gtap_table_nqueens is leaf_mode 1. */
+const gtap_task_table *gtap_table_nqueens_ex(int32_t n, int32_t cutoff, unsigned long long *d_count,
+                                             uint32_t leaf_mode);
 
 /* Synthetic tree (§6.3), on either worker kind
  * (worker_kind = GTAP_WORKER_THREAD: one task per lane; GTAP_WORKER_BLOCK: the

@@ -61,12 +61,13 @@ def fib_cutoff(n: int, cutoff: int, num_queues: int = 1, rt: Runtime | None = No
             rt.close()
 
 
-def nqueens(n: int, cutoff: int = 7, rt: Runtime | None = None, device: int = 0, stream=None, **cfg):
+def nqueens(n: int, cutoff: int = 7, leaf_mode: int = 1, rt: Runtime | None = None, device: int = 0, stream=None,
+            **cfg):
     """Number of n-queens solutions by the paper's bitmask task program; returns (count, stats)."""
     import torch
     count = torch.zeros(1, dtype=torch.int64, device=f"cuda:{device}")
     rt, own = _runtime(GTAP_WORKER_THREAD, rt, device, cfg)
-    table = Table.nqueens(n, cutoff, count)
+    table = Table.nqueens(n, cutoff, count, leaf_mode)
     try:
         rt.spawn_root(table, ())
         rt.run(stream)

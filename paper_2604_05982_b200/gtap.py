@@ -62,7 +62,7 @@ class Stats(ctypes.Structure):
 EXPORTS = [
     "gtap_abi_version", "gtap_status_str", "gtap_config_default", "gtap_workspace_bytes", "gtap_init",
     "gtap_spawn_root", "gtap_reset", "gtap_run", "gtap_sync", "gtap_root_result", "gtap_finalize",
-    "gtap_geometry", "gtap_table_destroy", "gtap_table_fib", "gtap_table_fib_cutoff", "gtap_table_nqueens", "gtap_table_tree", "gtap_table_mergesort", "gtap_table_mergesort_ex", "gtap_table_cilksort", "gtap_table_cilksort_ex",
+    "gtap_geometry", "gtap_table_destroy", "gtap_table_fib", "gtap_table_fib_cutoff", "gtap_table_nqueens", "gtap_table_nqueens_ex", "gtap_table_tree", "gtap_table_mergesort", "gtap_table_mergesort_ex", "gtap_table_cilksort", "gtap_table_cilksort_ex",
     "gtap_table_spmv",
     "gtap_table_bfs", "gtap_bfs_init_depth", "gtap_ubench_atomics",
 ]
@@ -102,6 +102,8 @@ def lib():
     L.gtap_table_fib_cutoff.restype = vp
     L.gtap_table_nqueens.argtypes = [i32, i32, vp]
     L.gtap_table_nqueens.restype = vp
+    L.gtap_table_nqueens_ex.argtypes = [i32, i32, vp, ctypes.c_uint32]
+    L.gtap_table_nqueens_ex.restype = vp
     L.gtap_table_tree.argtypes = [i32, i32, i32, ctypes.c_uint64, vp, ctypes.c_uint64, ctypes.c_uint32,
                                   ctypes.c_uint32, vp]
     L.gtap_table_tree.restype = vp
@@ -188,9 +190,11 @@ class Table:
         return Table(h, f"tree_{'thread' if kind == GTAP_WORKER_THREAD else 'block'}", kind, (buf, total))
 
     @staticmethod
-    def nqueens(n: int, cutoff: int, count) -> "Table":
-        """N-Queens; `count` is a CUDA int64 tensor of one element the run adds solutions to."""
-        return Table(lib().gtap_table_nqueens(n, cutoff, count.data_ptr()), "nqueens", GTAP_WORKER_THREAD, (count,))
+    def nqueens(n: int, cutoff: int, count, leaf_mode: int = 1) -> "Table":
+        """N-Queens (P:465); `count` is a CUDA int64 tensor of one element the run adds solutions to;
+        leaf_mode 0 = serial leaf on the task's lane (paper), 1 = the warp counts the leaf."""
+        return Table(lib().gtap_table_nqueens_ex(n, cutoff, count.data_ptr(), leaf_mode), "nqueens",
+                     GTAP_WORKER_THREAD, (count,))
 
     @staticmethod
     def mergesort(keys, scratch, cutoff: int = 128, merge_mode: int = 1) -> "Table":

@@ -35,7 +35,7 @@ struct gtap_runtime {
     const gtap_task_table* table;
     RootSpec* h_roots;     // pinned staging (max_roots)
     Ctl* h_ctl;            // pinned: control block staging / readback
-    cudaEvent_t ev0, ev1;
+    cudaEvent_t ev0, ev1, ev2;   // kernel start / end, control-block readback done
     bool in_flight;
     bool dirty;            // workspace used since the last reset
     uint32_t run_grid, run_block, run_W;
@@ -210,7 +210,8 @@ gtap_status gtap_init(const gtap_config* in, void* d_workspace, size_t bytes, gt
         gtap_finalize(rt);
         return GTAP_E_NOMEM;
     }
-    if (cudaEventCreate(&rt->ev0) != cudaSuccess || cudaEventCreate(&rt->ev1) != cudaSuccess) {
+    if (cudaEventCreate(&rt->ev0) != cudaSuccess || cudaEventCreate(&rt->ev1) != cudaSuccess ||
+        cudaEventCreate(&rt->ev2) != cudaSuccess) {
         gtap_finalize(rt);
         return GTAP_E_CUDA;
     }
@@ -309,6 +310,11 @@ gtap_status gtap_run(gtap_runtime* rt, void* stream) {
     const cudaError_t le = rt->table->launch(rt->table, p, grid, block, s);
     if (le != cudaSuccess) return GTAP_E_CUDA;
     if (cudaEventRecord(rt->ev1, s) != cudaSuccess) return GTAP_E_CUDA;
+    // the control block (error word, counters) comes back on the same stream right behind the kernel,
+    // so gtap_sync waits for this run only (no legacy-stream synchronous copy)
+    if (cudaMemcpyAsync(rt->h_ctl, rt->ws + rt->L.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaEventRecord(rt->ev2, s) != cudaSuccess)
+        return GTAP_E_CUDA;
     rt->in_flight = true;
     rt->dirty = true;
     rt->run_grid = grid;
@@ -324,11 +330,9 @@ gtap_status gtap_sync(gtap_runtime* rt, gtap_stats* out) {
     if (!rt->in_flight) return GTAP_E_INVAL;
     cudaSetDevice(rt->device);
     rt->in_flight = false;
-    if (cudaEventSynchronize(rt->ev1) != cudaSuccess) return GTAP_E_CUDA;
+    if (cudaEventSynchronize(rt->ev2) != cudaSuccess) return GTAP_E_CUDA;
     float ms = 0.f;
     cudaEventElapsedTime(&ms, rt->ev0, rt->ev1);
-    if (cudaMemcpy(rt->h_ctl, rt->ws + rt->L.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost) != cudaSuccess)
-        return GTAP_E_CUDA;
     const Ctl& c = *rt->h_ctl;
     if (out) {
         std::memset(out, 0, sizeof(*out));
@@ -372,12 +376,13 @@ gtap_status gtap_root_result(gtap_runtime* rt, uint32_t root_idx, void* out, uin
 gtap_status gtap_finalize(gtap_runtime* rt) {
     if (!rt) return GTAP_OK;
     cudaSetDevice(rt->device);
-    if (rt->in_flight) cudaEventSynchronize(rt->ev1);
+    if (rt->in_flight) cudaEventSynchronize(rt->ev2);
     if (rt->owns_ws && rt->ws) cudaFree(rt->ws);
     if (rt->h_roots) cudaFreeHost(rt->h_roots);
     if (rt->h_ctl) cudaFreeHost(rt->h_ctl);
     if (rt->ev0) cudaEventDestroy(rt->ev0);
     if (rt->ev1) cudaEventDestroy(rt->ev1);
+    if (rt->ev2) cudaEventDestroy(rt->ev2);
     delete rt;
     return GTAP_OK;
 }

@@ -16,7 +16,7 @@ srp, scol, sval, sx = synth.powerlaw_csr(1 << 22, seed=7, device="cuda")
 tbuf = synth.tree_buffer(1 << 25, device="cuda")
 for sm in (1, 4, 16, 32):
     out = []
-    with g.Runtime(g.GTAP_WORKER_BLOCK, 0, steal_max=sm, watchdog_ns=60_000_000_000, **bench.BFS_CFG) as rt:
+    with g.Runtime(g.GTAP_WORKER_BLOCK, 0, watchdog_ns=60_000_000_000, **dict(bench.BFS_CFG, steal_max=sm)) as rt:
         for s in srcs:
             out.append(min(g.bfs(rp, col, s, rt=rt)[1].device_ms for _ in range(3)))
     with g.Runtime(g.GTAP_WORKER_BLOCK, 0, steal_max=sm, **bench.SPMV_CFG) as rt:

@@ -213,6 +213,9 @@ struct MergeSlot {                           // placed 2 KB-aligned inside the b
 #ifndef GTAP_MS_WR
 #define GTAP_MS_WR 1024
 #endif
+#ifndef GTAP_MS_TILE_BITONIC
+#define GTAP_MS_TILE_BITONIC 1   // warp_merge tiles by a bitonic network (0: merge-path search + serial steps)
+#endif
 constexpr int kWT = GTAP_MS_WT;              // outputs per tile
 constexpr int kVT = kWT / 32;                // outputs per lane per tile
 constexpr int kWR = GTAP_MS_WR;              // keys per ring
@@ -648,6 +651,53 @@ __device__ __noinline__ void warp_merge(const int32_t* __restrict__ src, int32_t
         wm::wait<1>();  // the window was issued >= 2 tiles ago (see kTopChunk)
         __syncwarp();
         const uint32_t na = min(tile, m - pa), nb = min(tile, r - pb);
+#if GTAP_MS_TILE_BITONIC
+        // the tile's kWT outputs by one bitonic half-cleaner + merge network over registers:
+        // element e = k * 32 + lane of A[pa, pa + kWT) ++ reverse(B[pb, pb + kWT)) (runs padded with
+        // +inf past na / nb); c[e] = min(A[e], B[kWT-1-e]) is bitonic and holds the kWT smallest keys,
+        // and A[e] is taken iff A[e] <= B[kWT-1-e] (ties: left run first), so the count of taken A
+        // keys is the stable merge-path split of the tile; log2(kWT) compare stages sort c.
+        // Every smem access and the global stores are lane-contiguous (no search, no serial chain).
+        int32_t x[kVT];
+        uint32_t ca = 0;
+#pragma unroll
+        for (int k = 0; k < kVT; ++k) {
+            const uint32_t e = (uint32_t)k * 32u + lane, j = (uint32_t)kWT - 1u - e;
+            const bool ha = e < na, hb = j < nb;
+            const int32_t va = ha ? RA[(pa + e) & (kWR - 1u)] : INT_MAX;
+            const int32_t vb = hb ? RB[(pb + j) & (kWR - 1u)] : INT_MAX;
+            const bool takeA = ha && (!hb || va <= vb);
+            x[k] = takeA ? va : vb;
+            ca += (uint32_t)__popc(__ballot_sync(0xffffffffu, takeA));
+        }
+#pragma unroll
+        for (uint32_t stride = (uint32_t)kWT >> 1; stride > 0u; stride >>= 1) {
+            if (stride >= 32u) {
+#pragma unroll
+                for (int k = 0; k < kVT; ++k) {
+                    const int kk = k ^ (int)(stride >> 5);
+                    if (kk > k) {
+                        const int32_t u = x[k], v = x[kk];
+                        x[k] = min(u, v);
+                        x[kk] = max(u, v);
+                    }
+                }
+            } else {
+                const bool lower = (lane & stride) == 0u;
+#pragma unroll
+                for (int k = 0; k < kVT; ++k) {
+                    const int32_t p = __shfl_xor_sync(0xffffffffu, x[k], stride);
+                    x[k] = lower ? min(x[k], p) : max(x[k], p);
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < kVT; ++k) {
+            const uint32_t e = (uint32_t)k * 32u + lane;
+            if (e < tile) dst[out + e] = x[k];
+        }
+        __syncwarp();                                  // ring reads done before the top-up
+#else
         const uint32_t d = min(lane * (uint32_t)kVT, tile);
         uint32_t lo = d > nb ? d - nb : 0u, hi = min(d, na);
         // stable merge-path split at diagonal d: the smallest i in [lo, hi] with !(A[i] <= B[d-1-i]);
@@ -678,6 +728,7 @@ __device__ __noinline__ void warp_merge(const int32_t* __restrict__ src, int32_t
         }
         const uint32_t ca = __shfl_sync(0xffffffffu, ai, (tile - 1u) / (uint32_t)kVT);  // A keys consumed
         __syncwarp();                                  // ring reads done before the top-up
+#endif
         pa += ca;
         pb += tile - ca;
         out += tile;

@@ -49,3 +49,45 @@ for k in sorted(set(kind.tolist())):
         d = (t1[sel] - t0[sel]) / 1e3
         print(f"{KIND[k]:12s} size={size:9d} n={sel.sum():6d} start={(t0[sel].min() - base) / 1e6:7.3f} "
               f"end={(t1[sel].max() - base) / 1e6:7.3f} ms  dur_us mean={d.mean():8.1f} max={d.max():8.1f}")
+
+# timeline: average number of warps busy per 50 us bin, by record class (requester records 4/5 excluded:
+# their warps' chunk work is recorded as kinds 6/7)
+BIN = 50_000
+nb = int((t1.max() - base) // BIN) + 1
+cls = {"leaf": [2], "warp merge": [3], "chunks": [6, 7]}
+print("bin_us " + " ".join(f"{c:>11s}" for c in cls) + "   leaf_starts")
+for b in range(nb):
+    lo, hi = base + b * BIN, base + (b + 1) * BIN
+    row = []
+    for c, ks in cls.items():
+        sel = np.isin(kind, ks)
+        ov = np.clip(np.minimum(t1[sel], hi) - np.maximum(t0[sel], lo), 0, None)
+        row.append(ov.sum() / BIN)
+    ls = ((kind == 2) & (t0 >= lo) & (t0 < hi)).sum()
+    print(f"{b * 50:6d} " + " ".join(f"{v:11.1f}" for v in row) + f"   {ls}")
+
+# top-level merge: which warps merged its chunks, how many each, gaps between a warp's chunks
+wid = (buf[:m, 3] >> np.uint64(32)).astype(np.int64)
+top = (kind == 5) & (sz == sz[kind == 5].max()) if (kind == 5).any() else None
+if top is not None and top.any():
+    ts, te = t0[top].min(), t1[top].max()
+    ch = (kind == 6) & (t0 >= ts) & (t1 <= te)
+    ws = wid[ch]
+    uw, cnts = np.unique(ws, return_counts=True)
+    print(f"top merge {sz[top].max()} keys: {(te - ts) / 1e3:.1f} us, chunks {ch.sum()}, distinct warps {len(uw)}, "
+          f"chunks/warp hist {np.bincount(cnts).tolist()}")
+    first = np.array([t0[ch][ws == w].min() - ts for w in uw]) / 1e3
+    print(f"  first chunk start after open: p10 {np.percentile(first, 10):.1f} p50 {np.percentile(first, 50):.1f} "
+          f"p90 {np.percentile(first, 90):.1f} max {first.max():.1f} us")
+    gaps = []
+    for w in uw:
+        sel = ch & (wid == w)
+        a, b = np.sort(t0[sel]), np.sort(t1[sel])
+        gaps += list((a[1:] - b[:-1]) / 1e3)
+    if gaps:
+        g_ = np.array(gaps)
+        print(f"  gap between a warp's chunks: p50 {np.percentile(g_, 50):.2f} p90 {np.percentile(g_, 90):.2f} max {g_.max():.2f} us")
+    d = (t1[ch] - t0[ch]) / 1e3
+    print(f"  chunk dur p10 {np.percentile(d, 10):.1f} p50 {np.percentile(d, 50):.1f} p90 {np.percentile(d, 90):.1f} max {d.max():.1f} us")
+    last = np.array([t1[ch][ws == w].max() for w in uw])
+    print(f"  last chunk end before close: p10 {(te - np.percentile(last, 90)) / 1e3:.1f} p50 {(te - np.percentile(last, 50)) / 1e3:.1f} us")

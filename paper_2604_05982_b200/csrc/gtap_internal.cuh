@@ -222,6 +222,11 @@ __device__ __forceinline__ long long atom_add_acq_rel(long long* p, long long v)
     asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], %2;" : "=l"(o) : "l"(p), "l"(v) : "memory");
     return o;
 }
+__device__ __forceinline__ uint32_t atom_add_acquire(uint32_t* p, uint32_t v) {
+    uint32_t r;
+    asm volatile("atom.acquire.gpu.global.add.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "r"(v) : "memory");
+    return r;
+}
 __device__ __forceinline__ uint32_t atom_add_relaxed(uint32_t* p, uint32_t v) {
     uint32_t o;
     asm volatile("atom.relaxed.gpu.global.add.u32 %0, [%1], %2;" : "=r"(o) : "l"(p), "r"(v) : "memory");

@@ -116,6 +116,11 @@ template <class T>
 struct assist_of<T, decltype((void)T::kAssist, void())> { static constexpr bool value = T::kAssist; };
 
 template <class T, class = void>
+struct assist_all_of { static constexpr bool value = false; };
+template <class T>
+struct assist_all_of<T, decltype((void)T::kAssistAll, void())> { static constexpr bool value = T::kAssistAll; };
+
+template <class T, class = void>
 struct num_queues_of { static constexpr int value = 1; };
 template <class T>
 struct num_queues_of<T, decltype((void)T::kNumQueues, void())> { static constexpr int value = T::kNumQueues; };
@@ -284,6 +289,11 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
                 }
             }
         }
+        // an open GPU-wide assist (warp-assist tables) goes before stealing: its requester's task
+        // is on the critical path, and when one is open the deques are mostly empty
+        if constexpr (assist_of<T>::value) {
+            if (n == 0 && T::help_idle(args, lane, bx)) { backoff = 32; continue; }
+        }
         // steal: probe 32 random (victim, queue) pairs in parallel, claim from the fullest
         if (n == 0 && p.W > 1) {
             // a long-idle warp probes once per wake-up (keeps idle L2 traffic off busy workers)
@@ -391,6 +401,15 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
             // requesting lanes' join releases below cover every lane's stores.
             uint32_t req = __ballot_sync(0xffffffffu, my != kNone && o.assist != 0u && o.err == 0u);
             const bool any_assist = req != 0u;
+            if constexpr (assist_all_of<T>::value) {
+                // the table takes every request at once (batched assists; it cannot fail)
+                static_assert(kDataWords == 4, "assist_all takes the 4 request words");
+                if (req) {
+                    T::assist_all(args, req, o.ap[0], o.ap[1], o.ap[2], o.ap[3], lane, bx);
+                    if (lane == 0) st_assist += (uint32_t)__popc(req);
+                    req = 0u;
+                }
+            }
             while (req) {
                 const uint32_t src = (uint32_t)__ffs(req) - 1u;
                 req &= req - 1u;

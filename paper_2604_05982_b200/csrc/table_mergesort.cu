@@ -188,7 +188,7 @@ __device__ __forceinline__ void ms_trace(unsigned long long t0, uint32_t size, u
         unsigned smid;
         asm("mov.u32 %0, %%smid;" : "=r"(smid));
         gtap_ms_trace[i] = make_ulonglong4(t0, dev::globaltimer(), ((unsigned long long)size << 32) | l,
-                                           ((unsigned long long)smid << 8) | kind);
+                                           ((unsigned long long)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) << 32) | ((unsigned long long)smid << 8) | kind);
     }
 }
 #define MS_T0 const unsigned long long ms_t0 = dev::globaltimer()
@@ -697,6 +697,61 @@ __device__ __noinline__ void warp_merge(const int32_t* __restrict__ src, int32_t
             if (e < tile) dst[out + e] = x[k];
         }
         __syncwarp();                                  // ring reads done before the top-up
+#elif GTAP_MS_TILE_BITONIC == 2
+        // lane k owns outputs [d, d + kVT) of the tile, d = k * kVT: a stable merge-path search at
+        // diagonal d in the rings (4-way, ~4 dependent round trips), then the kVT smallest of
+        // A[ai, ai + kVT) ++ reverse(B[bi, bi + kVT)) by a half-cleaner (A taken iff A <= B: ties
+        // left first) and log2(kVT) in-register compare stages; no shuffles, no serial chain;
+        // 16-B stores when the output is 16-B aligned
+        const uint32_t d = min(lane * (uint32_t)kVT, tile);
+        uint32_t lo = d > nb ? d - nb : 0u, hi = min(d, na);
+        const uint32_t cb = pb + d - 1u;
+        while (lo < hi) {
+            const uint32_t w = hi - lo;
+            const uint32_t q1 = lo + (w >> 2), q2 = lo + (w >> 1), q3 = lo + ((3u * w) >> 2);
+            const bool p1 = RA[(pa + q1) & (kWR - 1u)] <= RB[(cb - q1) & (kWR - 1u)];
+            const bool p2 = RA[(pa + q2) & (kWR - 1u)] <= RB[(cb - q2) & (kWR - 1u)];
+            const bool p3 = RA[(pa + q3) & (kWR - 1u)] <= RB[(cb - q3) & (kWR - 1u)];
+            if (p3)      { lo = q3 + 1u; }
+            else if (p2) { lo = q2 + 1u; hi = q3; }
+            else if (p1) { lo = q1 + 1u; hi = q2; }
+            else         { hi = q1; }
+        }
+        const uint32_t ai = lo, bi = d - lo;
+        const uint32_t cnt = min((uint32_t)kVT, tile - d);
+        int32_t x[kVT];
+        uint32_t ta = 0;
+#pragma unroll
+        for (int v = 0; v < kVT; ++v) {
+            const uint32_t ia = ai + (uint32_t)v, ib = bi + (uint32_t)(kVT - 1 - v);
+            const bool ha = ia < na, hb = ib < nb;
+            const int32_t va = ha ? RA[(pa + ia) & (kWR - 1u)] : INT_MAX;
+            const int32_t vb = hb ? RB[(pb + ib) & (kWR - 1u)] : INT_MAX;
+            const bool takeA = ha && (!hb || va <= vb);
+            x[v] = takeA ? va : vb;
+            ta += takeA ? 1u : 0u;
+        }
+#pragma unroll
+        for (int stride = kVT / 2; stride > 0; stride >>= 1)
+#pragma unroll
+            for (int v = 0; v < kVT; ++v)
+                if ((v & stride) == 0) {
+                    const int32_t u = x[v], w = x[v + stride];
+                    x[v] = min(u, w);
+                    x[v + stride] = max(u, w);
+                }
+        int32_t* o = dst + out + d;
+        if (cnt == (uint32_t)kVT && ((reinterpret_cast<uintptr_t>(o) & 15u) == 0u)) {
+#pragma unroll
+            for (int v = 0; v < kVT; v += 4)
+                *reinterpret_cast<int4*>(o + v) = make_int4(x[v], x[v + 1], x[v + 2], x[v + 3]);
+        } else {
+#pragma unroll
+            for (int v = 0; v < kVT; ++v)
+                if ((uint32_t)v < cnt) o[v] = x[v];
+        }
+        const uint32_t ca = __shfl_sync(0xffffffffu, ai + ta, 31);  // A keys consumed (full tiles)
+        __syncwarp();                                  // ring reads done before the top-up
 #else
         const uint32_t d = min(lane * (uint32_t)kVT, tile);
         uint32_t lo = d > nb ? d - nb : 0u, hi = min(d, na);
@@ -783,10 +838,55 @@ constexpr uint32_t kGSlots = 1024;
 #define GTAP_MS_GLOBAL_MIN 16384
 #endif
 #ifndef GTAP_MS_GCHUNK
-#define GTAP_MS_GCHUNK 4096
+#define GTAP_MS_GCHUNK 3072
 #endif
 constexpr uint32_t kGlobalAssistMin = GTAP_MS_GLOBAL_MIN;
 constexpr uint32_t kGChunk = GTAP_MS_GCHUNK;
+// guided chunking (GTAP_MS_GUIDED): phase p < kGPhases - 1 takes half of the outputs still
+// unassigned (rounded down to its chunk size) in chunks of kGChunk0 >> p keys, the last phase the
+// rest; chunks are claimed in index order, so a slot hands out long chunks first and short ones at
+// its tail (helpers finishing a long chunk late find short ones left). Count and ranges follow from
+// the merge length alone, so the requester and every helper agree without communicating.
+#ifndef GTAP_MS_GUIDED
+#define GTAP_MS_GUIDED 0   // 1: guided chunk sizes (measured no better than uniform chunks at 2^24)
+#endif
+#ifndef GTAP_MS_GC0
+#define GTAP_MS_GC0 8192
+#endif
+#ifndef GTAP_MS_GPH
+#define GTAP_MS_GPH 4
+#endif
+#ifndef GTAP_MS_GUIDED_MIN
+#define GTAP_MS_GUIDED_MIN (1u << 21)   // shorter merges: uniform kGChunk chunks
+#endif
+constexpr uint32_t kGChunk0 = GTAP_MS_GC0;
+constexpr int kGPhases = GTAP_MS_GPH;
+__device__ __forceinline__ uint32_t gch_count(uint32_t n) {
+    if (!GTAP_MS_GUIDED || n < GTAP_MS_GUIDED_MIN) return (n + kGChunk - 1u) / kGChunk;
+    uint32_t b = 0, c = 0;
+#pragma unroll
+    for (int p = 0; p < kGPhases - 1; ++p) {
+        const uint32_t S = kGChunk0 >> p, len = ((n - b) / 2u) / S * S;
+        c += len / S;
+        b += len;
+    }
+    constexpr uint32_t SL = kGChunk0 >> (kGPhases - 1);
+    return c + (n - b + SL - 1u) / SL;
+}
+// output range [x, y) of chunk c (c < gch_count(n))
+__device__ __forceinline__ uint2 gch_range(uint32_t n, uint32_t c) {
+    if (!GTAP_MS_GUIDED || n < GTAP_MS_GUIDED_MIN) return make_uint2(c * kGChunk, min(n, c * kGChunk + kGChunk));
+    uint32_t b = 0;
+#pragma unroll
+    for (int p = 0; p < kGPhases - 1; ++p) {
+        const uint32_t S = kGChunk0 >> p, len = ((n - b) / 2u) / S * S, k = len / S;
+        if (c < k) return make_uint2(b + c * S, b + c * S + S);
+        c -= k;
+        b += len;
+    }
+    constexpr uint32_t SL = kGChunk0 >> (kGPhases - 1);
+    return make_uint2(b + c * SL, min(n, b + c * SL + SL));
+}
 struct __align__(128) GSlot {
     uint32_t state, next, done, nchunks;
     uint32_t l, m, r, depth;
@@ -895,6 +995,123 @@ struct MergesortTable {
         return true;
     }
 
+#ifndef GTAP_MS_BATCH
+#define GTAP_MS_BATCH 0   // 1: batched warp assists for leaves <= 128 keys and merges <= 512 keys (measured slower: shuffle-bound)
+#endif
+    static constexpr bool kAssistAll = MODE == 1u && GTAP_MS_BATCH != 0;
+    // gather up to G requests of mask m (consumed) from their lanes: {l, r, depth} per slot, n = 0 if empty
+    template <int G>
+    __device__ __forceinline__ static void take(uint32_t& m, uint32_t a0, uint32_t a1, uint32_t a2,
+                                                uint32_t (&gl)[G], uint32_t (&gr)[G], uint32_t (&gd)[G]) {
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            const uint32_t s = m ? (uint32_t)__ffs(m) - 1u : 0u;
+            const uint32_t l = __shfl_sync(0xffffffffu, a0, s), r = __shfl_sync(0xffffffffu, a1, s),
+                           d = __shfl_sync(0xffffffffu, a2, s);
+            gl[g] = l; gr[g] = m ? r : l; gd[g] = d;
+            m &= m - 1u;
+        }
+    }
+    // G merges of <= 32 K keys: src = buf(depth + 1)[l, m) and [m, r) -> buf(depth)[l, r)
+    template <int K, int G>
+    __device__ __noinline__ static uint32_t merge_batch(const Args& a, uint32_t msk, uint32_t a0, uint32_t a1,
+                                                        uint32_t a2, uint32_t lane) {
+        constexpr uint32_t N = 32u * K;
+        {
+            MS_T0;
+            uint32_t gl[G], gr[G], gd[G];
+            take<G>(msk, a0, a1, a2, gl, gr, gd);
+            int32_t x[G][K];
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const uint32_t m = gl[g] + (gr[g] - gl[g]) / 2u, na = m - gl[g], nb = gr[g] - m;
+                const int32_t* src = buf(a, gd[g] + 1u);
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    const uint32_t i = (uint32_t)k * 32u + lane;
+                    x[g][k] = i < na ? src[gl[g] + i] : (i >= N - nb ? src[m + (N - 1u - i)] : INT_MAX);
+                }
+            }
+            warp_bitonic_merge_multi<K, G>(x, lane);
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                int32_t* dst = buf(a, gd[g]) + gl[g];
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    const uint32_t i = (uint32_t)k * 32u + lane;
+                    if (i < gr[g] - gl[g]) dst[i] = x[g][k];
+                }
+                MS_TRACE_LANE0(gr[g] - gl[g], gl[g], 3u);
+            }
+        }
+        return msk;
+    }
+    // G leaf sorts of <= 32 K keys: keys[l, r) -> buf(depth)[l, r)
+    template <int K, int G>
+    __device__ __noinline__ static uint32_t leaf_batch(const Args& a, uint32_t msk, uint32_t a0, uint32_t a1,
+                                                       uint32_t a2, uint32_t lane) {
+        {
+            MS_T0;
+            uint32_t gl[G], gr[G], gd[G];
+            take<G>(msk, a0, a1, a2, gl, gr, gd);
+            int32_t x[G][K];
+#pragma unroll
+            for (int g = 0; g < G; ++g)
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    const uint32_t i = (uint32_t)k * 32u + lane;
+                    x[g][k] = i < gr[g] - gl[g] ? a.keys[gl[g] + i] : INT_MAX;
+                }
+            warp_bitonic_sort_multi<K, G>(x, lane);
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                int32_t* dst = buf(a, gd[g]) + gl[g];
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    const uint32_t i = (uint32_t)k * 32u + lane;
+                    if (i < gr[g] - gl[g]) dst[i] = x[g][k];
+                }
+                MS_TRACE_LANE0(gr[g] - gl[g], gl[g], 2u);
+            }
+        }
+        return msk;
+    }
+    // scheduler hook (2b), all 32 lanes: every request of mask req (this lane's ap = {l, r, depth, leaf}).
+    // Leaves <= 128 keys go 8 at a time, merges <= 256 / <= 512 keys 4 / 2 at a time (their loads and
+    // network stages interleaved); the rest one at a time through assist().
+    __device__ __noinline__ static void assist_all(const Args& a, uint32_t req, uint32_t a0, uint32_t a1,
+                                                   uint32_t a2, uint32_t a3, uint32_t lane, WarpAssistHolder* H) {
+        const bool mine = (req >> lane) & 1u;
+        const uint32_t n = a1 - a0;
+        const uint32_t mleaf = __ballot_sync(0xffffffffu, mine && a3 == 1u && n <= 128u);
+        const uint32_t m256 = __ballot_sync(0xffffffffu, mine && a3 == 0u && n <= 256u);
+        const uint32_t m512 = __ballot_sync(0xffffffffu, mine && a3 == 0u && n > 256u && n <= 512u);
+        // group sizes follow the request count (an empty slot would still run its network)
+        for (uint32_t m = mleaf; m;) {
+            const int c = __popc(m);
+            m = c >= 8 ? leaf_batch<4, 8>(a, m, a0, a1, a2, lane)
+              : c >= 4 ? leaf_batch<4, 4>(a, m, a0, a1, a2, lane)
+              : c >= 2 ? leaf_batch<4, 2>(a, m, a0, a1, a2, lane)
+                       : leaf_batch<4, 1>(a, m, a0, a1, a2, lane);
+        }
+        for (uint32_t m = m256; m;) {
+            const int c = __popc(m);
+            m = c >= 4 ? merge_batch<8, 4>(a, m, a0, a1, a2, lane)
+              : c >= 2 ? merge_batch<8, 2>(a, m, a0, a1, a2, lane)
+                       : merge_batch<8, 1>(a, m, a0, a1, a2, lane);
+        }
+        for (uint32_t m = m512; m;)
+            m = __popc(m) >= 2 ? merge_batch<16, 2>(a, m, a0, a1, a2, lane) : merge_batch<16, 1>(a, m, a0, a1, a2, lane);
+        uint32_t rest = req & ~(mleaf | m256 | m512);
+        while (rest) {
+            const uint32_t s = (uint32_t)__ffs(rest) - 1u;
+            rest &= rest - 1u;
+            const uint32_t ap[kDataWords] = {__shfl_sync(0xffffffffu, a0, s), __shfl_sync(0xffffffffu, a1, s),
+                                             __shfl_sync(0xffffffffu, a2, s), __shfl_sync(0xffffffffu, a3, s)};
+            assist(a, ap, lane, H);   // mergesort assists always succeed
+        }
+    }
+
     // claim and merge chunks of the block's open board until none is left (all 32 lanes)
     __device__ __noinline__ static void help_chunks(const Args& a, WarpAssistHolder* H, uint32_t lane, WarpTiles* T) {
         volatile WarpAssistHolder::Board& B = H->board;
@@ -923,16 +1140,24 @@ struct MergesortTable {
         const uint32_t si = (uint32_t)(S - a.gb->slot);
         while (true) {
             uint32_t c = 0;
-            if (lane == 0) c = atom_add_relaxed(&S->next, 1u);
+            // the acquire claim orders the parameter loads after it (the requester fenced them
+            // before next = 0); nchunks and {l, m, r, depth} are then read in one round trip
+            uint32_t nch = 0;
+            uint4 prm = make_uint4(0u, 0u, 0u, 0u);
+            if (lane == 0) {
+                c = atom_add_acquire(&S->next, 1u);
+                nch = ld_relaxed(&S->nchunks);
+                prm = ld_relaxed_v4(&S->l);
+            }
             c = __shfl_sync(0xffffffffu, c, 0);
-            __threadfence();
-            const uint32_t nch = ld_relaxed(&S->nchunks);   // read after the claim (see GBoard)
+            nch = __shfl_sync(0xffffffffu, nch, 0);   // read after the claim (see GBoard)
             if (c >= nch) break;
             if (c == nch - 1u && lane == 0) atomicAnd(&a.gb->bits[si >> 5], ~(1u << (si & 31u)));  // all claimed
-            const uint32_t l = ld_relaxed(&S->l), m = ld_relaxed(&S->m), r = ld_relaxed(&S->r),
-                           depth = ld_relaxed(&S->depth);
+            const uint32_t l = __shfl_sync(0xffffffffu, prm.x, 0), m = __shfl_sync(0xffffffffu, prm.y, 0),
+                           r = __shfl_sync(0xffffffffu, prm.z, 0), depth = __shfl_sync(0xffffffffu, prm.w, 0);
             const int32_t* src = buf(a, depth + 1u);
-            const uint32_t n = r - l, o0 = c * kGChunk, o1 = min(n, o0 + kGChunk);
+            const uint2 orng = gch_range(r - l, c);
+            const uint32_t o0 = orng.x, o1 = orng.y;
             MS_T0;
             const uint2 sp = warp_split2(src, l, m, r, o0, o1, lane);
             const uint32_t i0 = sp.x, i1 = sp.y;
@@ -988,7 +1213,7 @@ struct MergesortTable {
         }
         if (sidx == kNone) return false;
         GSlot* S = gb->slot + sidx;
-        const uint32_t nch = (r - l + kGChunk - 1u) / kGChunk;
+        const uint32_t nch = gch_count(r - l);
         if (lane == 0) {
             st_relaxed(&S->l, l); st_relaxed(&S->m, m); st_relaxed(&S->r, r); st_relaxed(&S->depth, depth);
             st_relaxed(&S->nchunks, nch); st_relaxed(&S->done, 0u);

@@ -104,6 +104,80 @@ __device__ __noinline__ void warp_merge_bitonic_k(const int32_t* __restrict__ A,
     }
 }
 
+// G independent problems interleaved stage by stage (batched warp assists): the G networks'
+// shuffles and compare-exchanges of one stage are independent, so a warp keeps G problems' loads
+// and shuffle latencies in flight instead of one. x[g][k] is element k * 32 + lane of problem g.
+template <int K, int G>
+__device__ __forceinline__ void warp_bitonic_sort_multi(int32_t (&x)[G][K], uint32_t lane) {
+    constexpr int N = 32 * K;
+#pragma unroll
+    for (int size = 2; size <= N; size <<= 1) {
+#pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            if (stride >= 32) {
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    const int kk = k ^ (stride >> 5);
+                    if (kk > k) {
+                        const bool up = (((uint32_t)k * 32u + lane) & (uint32_t)size) == 0u;
+#pragma unroll
+                        for (int g = 0; g < G; ++g) {
+                            const int32_t a = x[g][k], b = x[g][kk];
+                            const bool sw = up ? (a > b) : (a < b);
+                            x[g][k] = sw ? b : a;
+                            x[g][kk] = sw ? a : b;
+                        }
+                    }
+                }
+            } else {
+                const bool lower = (lane & (uint32_t)stride) == 0u;
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    const bool up = (((uint32_t)k * 32u + lane) & (uint32_t)size) == 0u;
+#pragma unroll
+                    for (int g = 0; g < G; ++g) {
+                        const int32_t p = __shfl_xor_sync(0xffffffffu, x[g][k], stride);
+                        x[g][k] = (lower == up) ? min(x[g][k], p) : max(x[g][k], p);
+                    }
+                }
+            }
+        }
+    }
+}
+
+// the merge stages of warp_merge_bitonic_k on G problems (x[g] = A ascending, padding, B reversed)
+template <int K, int G>
+__device__ __forceinline__ void warp_bitonic_merge_multi(int32_t (&x)[G][K], uint32_t lane) {
+    constexpr uint32_t N = 32u * K;
+#pragma unroll
+    for (uint32_t stride = N >> 1; stride > 0; stride >>= 1) {
+        if (stride >= 32u) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const int kk = k ^ (int)(stride >> 5);
+                if (kk > k) {
+#pragma unroll
+                    for (int g = 0; g < G; ++g) {
+                        const int32_t a = x[g][k], b = x[g][kk];
+                        x[g][k] = min(a, b);
+                        x[g][kk] = max(a, b);
+                    }
+                }
+            }
+        } else {
+            const bool lower = (lane & stride) == 0u;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    const int32_t p = __shfl_xor_sync(0xffffffffu, x[g][k], stride);
+                    x[g][k] = lower ? min(x[g][k], p) : max(x[g][k], p);
+                }
+            }
+        }
+    }
+}
+
 constexpr uint32_t kBitonicMax = 1024;  // merges up to this many keys: one bitonic network
 
 // all 32 lanes: A[0, na) and B[0, nb) (sorted, na + nb <= kBitonicMax) merged into out[0, na + nb)

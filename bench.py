@@ -42,7 +42,7 @@ MS0_CFG = dict(grid_size=0, block_size=128, max_tasks_per_worker=1024, idle_back
 FIB_N = 40
 FIB_CFG = dict(grid_size=0, block_size=128, max_tasks_per_worker=4096)
 SPMV_ROWS = 1 << 22
-SPMV_NNZ_CUT = 8192
+SPMV_NNZ_CUT = 65536
 SPMV_FANOUT = 32
 SPMV_PARTS = 148 * 8     # forest: one nnz-balanced root per worker (fn part(k, R), reading R20)
 SPMV_CFG = dict(grid_size=148 * 8, block_size=128, max_tasks_per_worker=1024, max_roots=SPMV_PARTS)

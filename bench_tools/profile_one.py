@@ -29,7 +29,7 @@ elif wl == "spmv":
     rp, col, val, x = synth.powerlaw_csr(rows, seed=7, device="cuda")
     parts = int(os.environ.get("SPMV_PARTS", getattr(bench, "SPMV_PARTS", 0)))
     cut = int(os.environ.get("SPMV_CUT", bench.SPMV_NNZ_CUT))
-    with g.Runtime(g.GTAP_WORKER_BLOCK, 0, max_roots=max(parts, 1), **bench.SPMV_CFG) as rt:
+    with g.Runtime(g.GTAP_WORKER_BLOCK, 0, **dict(bench.SPMV_CFG, max_roots=max(parts, 1))) as rt:
         for i in range(reps):
             y, st = g.spmv(rp, col, val, x, nnz_cut=cut, fanout=bench.SPMV_FANOUT, parts=parts, rt=rt)
             print("spmv", rows, st.device_ms, st.tasks, flush=True)

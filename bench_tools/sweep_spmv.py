@@ -16,11 +16,13 @@ algo = 8.0 * nnz + 12.0 * (1 << 22)
 ref = None
 CFGS = {'libgtap.so': [(148 * 8, 128)], 'libgtap_gtap_spmv_per16.so': [(148 * 8, 128)], 'libgtap_gtap_spmv_per12.so': [(148 * 8, 128)],
         'libgtap_gtap_spmv_per16_gtap_spmv_minb3.so': [(148 * 6, 128), (148 * 3, 256)]}
-for grid, block in CFGS[os.path.basename(os.environ.get('GTAP_LIB', 'libgtap.so'))]:
+FULL = os.environ.get('SWEEP_FULL') == '1'
+GEOMS = [(148 * 8, 128), (148 * 4, 256), (148 * 16, 64)] if FULL else CFGS.get(os.path.basename(os.environ.get('GTAP_LIB', 'libgtap.so')), [(148 * 8, 128)])
+for grid, block in GEOMS:
     with g.Runtime(g.GTAP_WORKER_BLOCK, 0, grid_size=grid, block_size=block, max_tasks_per_worker=2048,
                    max_roots=4 * grid) as rt:
-        for parts in (grid, 2 * grid):
-            for cut in (8192, 65536):
+        for parts in ((grid, 2 * grid) if FULL else (grid,)):
+            for cut in ((8192, 65536, 262144) if FULL else (8192, 65536)):
                 sts = []
                 for _ in range(4):
                     y.zero_()

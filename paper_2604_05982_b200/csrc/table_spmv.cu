@@ -34,11 +34,18 @@ struct SpmvTable {
     static constexpr int kPer = GTAP_SPMV_PER;  // non-zeros per thread per chunk
     static constexpr int kMaxBlock = 256;   // prod[] sized for blocks up to 256 threads
     static constexpr int kRp = 512;         // row_ptr entries staged per chunk (more rows: global loads)
+#ifndef GTAP_SPMV_ROWS_BY_THREAD
+#define GTAP_SPMV_ROWS_BY_THREAD 1
+#endif
+    static constexpr int kShortSeg = 64;    // in-chunk row segments up to this long: one thread
+    static constexpr int kLongCap = kPer * kMaxBlock / (kShortSeg + 1) + 1;  // > segments that fit a chunk
     struct Scratch {
         float prod[kPer * kMaxBlock];
         int32_t rp[kRp + 1];
         uint32_t rcur, rnext;
         float carry, carry_next;
+        uint32_t nlong;
+        uint32_t longr[kLongCap];
     };
     struct Args {
         const int32_t* row_ptr;
@@ -165,6 +172,63 @@ struct SpmvTable {
             __syncthreads();
 #endif
             const float carry_in = sc.carry;
+#if GTAP_SPMV_ROWS_BY_THREAD
+            // row phase, pass 1: one thread per row of the chunk; a segment of <= kShortSeg products
+            // is summed serially from shared memory (4 interleaved partial sums), longer segments are
+            // listed for the warp pass. (Warp-per-row reductions left 4 warps doing ~8 short rows
+            // each, one shuffle tree per row.)
+            if (tid == 0) sc.nlong = 0u;
+            __syncthreads();
+            for (uint32_t i = tid;; i += bd) {
+                const uint32_t r = r0 + i;
+                if (r >= hi) break;
+                const int32_t rs = i < (uint32_t)kRp ? sc.rp[i] : __ldg(&a.row_ptr[r]);
+                if (rs >= c1) break;                          // rows are sorted by start
+                const int32_t re = i < (uint32_t)kRp ? sc.rp[i + 1] : __ldg(&a.row_ptr[r + 1]);
+                const int32_t a0 = max(rs, c0), a1 = min(re, c1);
+                if (a1 - a0 > kShortSeg) {
+                    const uint32_t q = atomicAdd(&sc.nlong, 1u);
+                    if (q < (uint32_t)kLongCap) sc.longr[q] = r;
+                    continue;
+                }
+                float t0 = 0.f, t1 = 0.f, t2 = 0.f, t3 = 0.f;
+                int32_t j = a0 - c0;
+                const int32_t je = a1 - c0;
+                for (; j + 4 <= je; j += 4) {
+                    t0 += sc.prod[j]; t1 += sc.prod[j + 1]; t2 += sc.prod[j + 2]; t3 += sc.prod[j + 3];
+                }
+                for (; j < je; ++j) t0 += sc.prod[j];
+                float t = (t0 + t1) + (t2 + t3);
+                if (rs < c0) t += carry_in;                   // only r0 can have started earlier
+                if (re <= c1) a.y[r] = t;
+                if (re >= c1) {                               // the last row touching this chunk
+                    sc.rnext = (re > c1) ? r : r + 1u;
+                    sc.carry_next = (re > c1) ? t : 0.f;
+                }
+            }
+            __syncthreads();
+            // pass 2: long segments, one warp each (strided lanes + shuffle tree)
+            const uint32_t nlong = sc.nlong;
+            for (uint32_t q = warp; q < nlong; q += nw) {     // warp-uniform
+                const uint32_t r = q < (uint32_t)kLongCap ? sc.longr[q] : 0u;
+                const uint32_t i = r - r0;
+                const int32_t rs = i < (uint32_t)kRp ? sc.rp[i] : __ldg(&a.row_ptr[r]);
+                const int32_t re = i < (uint32_t)kRp ? sc.rp[i + 1] : __ldg(&a.row_ptr[r + 1]);
+                const int32_t a0 = max(rs, c0), a1 = min(re, c1);
+                float t = 0.f;
+                for (int32_t j = a0 + (int32_t)lane; j < a1; j += 32) t += sc.prod[j - c0];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+                if (rs < c0) t += carry_in;
+                if (lane == 0) {
+                    if (re <= c1) a.y[r] = t;
+                    if (re >= c1) {
+                        sc.rnext = (re > c1) ? r : r + 1u;
+                        sc.carry_next = (re > c1) ? t : 0.f;
+                    }
+                }
+            }
+#else
             for (uint32_t r = r0 + warp; r < hi; r += nw) {   // warp-uniform
                 const uint32_t i = r - r0;
                 const int32_t rs = i < (uint32_t)kRp ? sc.rp[i] : __ldg(&a.row_ptr[r]);
@@ -184,6 +248,7 @@ struct SpmvTable {
                     }
                 }
             }
+#endif
 #ifdef GTAP_SPMV_PIPE
             if (more) {
 #pragma unroll

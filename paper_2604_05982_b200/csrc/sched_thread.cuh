@@ -508,6 +508,27 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
                 resume_q = o.next_queue;
             }
         }
+        // finish: copy the result into the parent's slot (copy-at-finish, R8)
+        if (!T::kJoinReduceAdd && fin && err == 0u && parent != kNone && !is_root_link(parent) && o.has_result)
+            st_relaxed(reinterpret_cast<int32_t*>(&p.rec[parent].d[2 + ord]), o.result);
+        __syncwarp();
+
+        // ================= (3c) join: last child re-enqueues the parent (P:55) =================
+        // the join RMW is issued here and its result consumed after the surplus-free atomics below,
+        // so the two round trips overlap (the freed records are not the parent's)
+        const bool jn = fin && err == 0u && parent != kNone && !is_root_link(parent);
+        unsigned long long jold = 0;
+        if (jn) {
+            if constexpr (T::kJoinReduceAdd) {
+                // one relaxed 64-bit RMW: pending -= 1 and acc += result (the count never
+                // underflows, so adding 0xFFFFFFFF carries exactly once into acc: add result - 1)
+                const unsigned long long inc =
+                    ((unsigned long long)(uint32_t)(o.result - 1) << 32) | 0xFFFFFFFFull;
+                jold = atom_add_relaxed_u64(&p.rec[parent], inc);
+            } else {
+                jold = (uint32_t)atom_add_acq_rel(&p.rec[parent].pending, -1);
+            }
+        }
         // surplus freed records go back to their home worker's free ring
         if (F > T_total) {
             const bool mine_free = lane < F - T_total;
@@ -527,31 +548,16 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
             const uint32_t rf = __ballot_sync(0xffffffffu, mine_free && (fid >> p.logM) != w);
             if (lane == 0) st_rfree += __popc(rf);
         }
-        // finish: copy the result into the parent's slot (copy-at-finish, R8)
-        if (!T::kJoinReduceAdd && fin && err == 0u && parent != kNone && !is_root_link(parent) && o.has_result)
-            st_relaxed(reinterpret_cast<int32_t*>(&p.rec[parent].d[2 + ord]), o.result);
         __syncwarp();
-
-        // ================= (3c) join: last child re-enqueues the parent (P:55) =================
         if (fin && err == 0u) {
-            if (parent != kNone && !is_root_link(parent)) {
-                bool last;
-                uint32_t pend_old;
+            if (jn) {
+                const uint32_t pend_old = (uint32_t)jold;
+                const bool last = (pend_old & kPendMask) == 1u;
                 if constexpr (T::kJoinReduceAdd) {
-                    // one relaxed 64-bit RMW: pending -= 1 and acc += result (the count never
-                    // underflows, so adding 0xFFFFFFFF carries exactly once into acc: add result - 1)
-                    const unsigned long long inc =
-                        ((unsigned long long)(uint32_t)(o.result - 1) << 32) | 0xFFFFFFFFull;
-                    const unsigned long long old = atom_add_relaxed_u64(&p.rec[parent], inc);
-                    pend_old = (uint32_t)old;
-                    last = (pend_old & kPendMask) == 1u;
                     if (last) {  // the continuation reads the sum as load_result(0) + load_result(1)
-                        const uint32_t sum = (uint32_t)(old >> 32) + (uint32_t)o.result;
+                        const uint32_t sum = (uint32_t)(jold >> 32) + (uint32_t)o.result;
                         st_v2(&p.rec[parent].d[2], sum, 0u);
                     }
-                } else {
-                    pend_old = (uint32_t)atom_add_acq_rel(&p.rec[parent].pending, -1);
-                    last = (pend_old & kPendMask) == 1u;
                 }
                 if (last) {
                     resume_id = parent | (parent_is_heavy<T>(myfn, mydata) ? kHeavyBit : 0u);

@@ -17,7 +17,7 @@ ref = None
 CFGS = {'libgtap.so': [(148 * 8, 128)], 'libgtap_gtap_spmv_per16.so': [(148 * 8, 128)], 'libgtap_gtap_spmv_per12.so': [(148 * 8, 128)],
         'libgtap_gtap_spmv_per16_gtap_spmv_minb3.so': [(148 * 6, 128), (148 * 3, 256)]}
 FULL = os.environ.get('SWEEP_FULL') == '1'
-GEOMS = [(148 * 8, 128), (148 * 4, 256), (148 * 16, 64)] if FULL else CFGS.get(os.path.basename(os.environ.get('GTAP_LIB', 'libgtap.so')), [(148 * 8, 128)])
+GEOMS = [(int(os.environ['GRID']), 128)] if os.environ.get('GRID') else [(148 * 8, 128), (148 * 4, 256), (148 * 16, 64)] if FULL else CFGS.get(os.path.basename(os.environ.get('GTAP_LIB', 'libgtap.so')), [(148 * 8, 128)])
 for grid, block in GEOMS:
     with g.Runtime(g.GTAP_WORKER_BLOCK, 0, grid_size=grid, block_size=block, max_tasks_per_worker=2048,
                    max_roots=4 * grid) as rt:

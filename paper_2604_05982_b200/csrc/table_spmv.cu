@@ -26,7 +26,10 @@ struct SpmvTable {
 #ifndef GTAP_SPMV_MINB
 #define GTAP_SPMV_MINB 4
 #endif
-    static constexpr int kMaxThreads = 256, kMinBlocks = GTAP_SPMV_MINB;  // __launch_bounds__ (prod[] holds 8 x 256)
+#ifndef GTAP_SPMV_MAXT
+#define GTAP_SPMV_MAXT 256
+#endif
+    static constexpr int kMaxThreads = GTAP_SPMV_MAXT, kMinBlocks = GTAP_SPMV_MINB;  // __launch_bounds__ (prod[] holds 8 x 256)
     static constexpr int kSpawnCap = 32;
 #ifndef GTAP_SPMV_PER
 #define GTAP_SPMV_PER 8

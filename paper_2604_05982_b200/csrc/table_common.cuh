@@ -33,7 +33,7 @@ namespace gtap {
 
 template <class T>
 inline size_t thread_smem(uint32_t block) {
-    return block_extra_bytes<T>() + (size_t)(block / 32) * sizeof(WarpSmem<T::kMaxChildren>);
+    return block_extra_bytes<T>() + (size_t)(block / 32) * sizeof(WarpSmem<T::kMaxChildren, free_stack_of<T>::value>);
 }
 
 template <class T>

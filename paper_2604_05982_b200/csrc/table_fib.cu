@@ -18,6 +18,10 @@ struct FibTable {
     static constexpr bool kHasHeavy = false;
     static constexpr uint32_t kNumFn = 1;
     static constexpr bool kJoinReduceAdd = true;  // see TaskRec
+#ifndef GTAP_FIB_FSTACK
+#define GTAP_FIB_FSTACK 1024  // own free-stack depth (fib(40): 64 -> 13.1 ms, 256 -> 12.66, 1024 -> 12.45)
+#endif
+    static constexpr int kFreeStack = GTAP_FIB_FSTACK;
 #ifndef GTAP_FIB_MINB
 #define GTAP_FIB_MINB 3  // 72 regs, no spills (4: 64 regs + spills, 2% slower)
 #endif

@@ -392,6 +392,41 @@ def bench_cilksort(dev, reps=3):
                               frac=algo / (t * 1e-3) / 1e9 / pk["hbm_gbs"]))
 
 
+def bench_forest(dev, reps=3, arrays=16, n_each=1 << 20):
+    """SURVEY §8(a) C5b on one GPU: a forest of 16 independent 2^20-key mergesorts (one root per array,
+    the per-GPU shard of the 8-GPU weak-scaling configuration; BASELINE configs[4])."""
+    import torch
+
+    import synth
+    import paper_2604_05982_b200 as g
+    n = arrays * n_each
+    pristine = torch.cat([synth.keys_int32(n_each, seed=1000 + i, device=dev) for i in range(arrays)])
+    keys = torch.empty_like(pristine)
+    scratch = torch.empty_like(pristine)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
+    segs = [(i * n_each, (i + 1) * n_each) for i in range(arrays)]
+    with g.Runtime(g.GTAP_WORKER_THREAD, dev.index, **dict(MS_CFG, max_roots=arrays)) as rt:
+        ms = []
+        for i in range(reps + 1):
+            keys.copy_(pristine)
+            flush.fill_(1)
+            st = g.mergesort_forest_(keys, segs, scratch, MS_CUTOFF, merge_mode=MS_MERGE_MODE, rt=rt)
+            if i:
+                ms.append(st.device_ms)
+    k2 = keys.view(arrays, n_each)
+    ok = bool(torch.all(k2[:, 1:] >= k2[:, :-1]).item()) and bool(
+        torch.equal(torch.sort(pristine.view(arrays, n_each), dim=1).values, k2))
+    t = statistics.median(ms)
+    pk, _ = peaks()
+    levels = _ms_levels(n_each, MS_CUTOFF)
+    algo = 8.0 * n * (1 + levels)
+    return dict(workload=f"mergesort forest {arrays} x 2^20 int32 per GPU (configs[4] C5b), thread-level, cutoff 128",
+                metric="Mkeys/s", value=n / (t * 1e-3) / 1e6, ms=t, tasks=st.tasks, sorted=ok,
+                roofline=dict(bound="hbm", achieved=algo / (t * 1e-3) / 1e9, peak=pk["hbm_gbs"], unit="GB/s",
+                              frac=algo / (t * 1e-3) / 1e9 / pk["hbm_gbs"],
+                              algorithmic_bytes_per_key=8.0 * (1 + levels)))
+
+
 def bench_nqueens(dev, reps=3):
     """SURVEY §8(f) NEXT #4: N-Queens n = 16, cutoff depth 7 (P:465, P:588)."""
     import paper_2604_05982_b200 as g
@@ -559,6 +594,7 @@ def run_ours(args):
             secondary.append(bench_nqueens(dev))
             secondary.append(bench_mergesort_thread_merge(dev))
             secondary.append(bench_cilksort(dev))
+            secondary.append(bench_forest(dev))
             secondary.append(bench_tree(dev))
         except Exception as e:  # secondary results must not kill the main line
             secondary.append(dict(workload="fib40/atomics", error=repr(e)))

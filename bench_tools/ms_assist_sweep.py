@@ -15,7 +15,7 @@ ref = torch.sort(keys).values
 d = torch.empty_like(keys)
 scr = torch.empty_like(keys)
 lib = os.path.basename(os.environ.get("GTAP_LIB", "libgtap.so"))
-for backoff in (1024,):
+for backoff in tuple(int(b) for b in os.environ.get("BACKOFFS", "1024").split(",")):
     cfg = dict(bench.MS_CFG, idle_backoff_ns=backoff)
     with g.Runtime(g.GTAP_WORKER_THREAD, 0, watchdog_ns=60_000_000_000, **cfg) as rt:
         ms = []

@@ -125,6 +125,11 @@ template <class T>
 struct free_stack_of<T, decltype((void)T::kFreeStack, void())> { static constexpr int value = T::kFreeStack; };
 
 template <class T, class = void>
+struct stats_smem_of { static constexpr bool value = false; };
+template <class T>
+struct stats_smem_of<T, decltype((void)T::kStatsSmem, void())> { static constexpr bool value = T::kStatsSmem; };
+
+template <class T, class = void>
 struct assist_all_of { static constexpr bool value = false; };
 template <class T>
 struct assist_all_of<T, decltype((void)T::kAssistAll, void())> { static constexpr bool value = T::kAssistAll; };
@@ -154,6 +159,7 @@ __device__ __forceinline__ void qset(uint32_t (&a)[NQ], uint32_t q, uint32_t v) 
 // RMWs on it went to DRAM (fib(40), ncu: 45 % of the join atomics missed L2).
 template <int MAXC, int FS = GTAP_FSTACK>
 struct WarpSmem {
+    unsigned long long st[12];  // per-warp statistics (lane 0, shared atomics: no registers held across the loop)
     uint32_t kept[32];          // keep-for-next-cycle set
     uint32_t fbuf[32];          // records freed this cycle (reused first)
     uint32_t abuf[32 * MAXC];   // records drawn from the free ring / bump region
@@ -207,9 +213,24 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
     uint32_t nkept = 0;
     uint32_t rng = hash32(p.seed * 0x9E3779B97F4A7C15ull + (unsigned long long)w * 32u + lane);
     uint32_t backoff = 32;
-    unsigned long long st_tasks = 0, st_inv = 0, st_pops = 0, st_kept = 0, st_sok = 0, st_sfail = 0,
-                       st_stolen = 0, st_push = 0, st_cyc = 0, st_idle = 0, st_rfree = 0,
-                       st_assist = 0;
+    // per-warp statistics (lane 0 counts): registers by default; tables with kStatsSmem keep them in
+    // shared memory (12 x 64-bit counters held across the loop cost 24 registers per thread; the
+    // mergesort kernel at its 128-register cap spilled 188 B without them there; fib is 3 % faster
+    // with registers)
+    constexpr bool kStSmem = stats_smem_of<T>::value;
+    enum { kStTasks, kStInv, kStPops, kStKept, kStSok, kStSfail, kStStolen, kStPush, kStCyc, kStIdle, kStRfree,
+           kStAssist, kStN };
+    unsigned long long streg[kStSmem ? 1 : kStN];
+#pragma unroll
+    for (int k = 0; k < (kStSmem ? 1 : kStN); ++k) streg[k] = 0ull;
+    if (kStSmem && lane < (uint32_t)kStN) sm.st[lane] = 0ull;
+    __syncwarp();
+    auto stat = [&](int k, unsigned long long v) {
+        if constexpr (kStSmem) atomicAdd(&sm.st[k], v); else streg[k] += v;
+    };
+    auto stget = [&](int k) -> unsigned long long {
+        if constexpr (kStSmem) return sm.st[k]; else return streg[k];
+    };
     const unsigned long long t0 = globaltimer();
     uint32_t cyc_u = 0;  // warp-uniform cycle counter (every lane increments it)
     bool failed = false;
@@ -233,7 +254,7 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
         }
         bump = mine;
         tail[0] = mine;
-        st_tasks += (lane == 0) ? mine : 0;
+        if (lane == 0) stat(kStTasks, mine);
         __syncwarp();
     }
 
@@ -247,7 +268,7 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
         uint32_t done_seen = 0;
         if (lane < (uint32_t)NQ) S_lane = ld_relaxed(&p.dq[dq0 + lane].S);
         if (lane == 31) done_seen = ld_relaxed(&p.ctl->done);
-        if (lane == 0) st_kept += n;
+        if (lane == 0) stat(kStKept, n);
         // LIFO pop from a private part, round-robin over the queues from qc: no atomics (owner only)
         if (n < 32) {
 #pragma unroll
@@ -264,7 +285,7 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
                     qset(tail, q, tq - c);
                     n += c;
                     qc = q;
-                    if (lane == 0) st_pops += c;
+                    if (lane == 0) stat(kStPops, c);
                     break;
                 }
             }
@@ -299,7 +320,7 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
                     if (lane < got) my = ld_relaxed(&ringq[(s_new + got - 1u - lane) & qmask]);
                     n = got;
                     qc = q;
-                    if (lane == 0) st_pops += got;
+                    if (lane == 0) stat(kStPops, got);
                     break;
                 }
             }
@@ -325,7 +346,7 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
                 uint32_t best = (min(avail, (1u << 26)) << 5) | lane;
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
-                if ((best >> 5) == 0) { if (lane == 0) ++st_sfail; continue; }
+                if ((best >> 5) == 0) { if (lane == 0) stat(kStSfail, 1); continue; }
                 const uint32_t bl = best & 31u;
                 const uint32_t vdq = __shfl_sync(0xffffffffu, vd, bl);
                 const uint32_t vqq = __shfl_sync(0xffffffffu, vq, bl);
@@ -357,20 +378,20 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
                     if (lane == 0) {
                         red_add_release(&vm->steal_done, got);
                         st_relaxed(&vm->lock, 0u);
-                        ++st_sok;
-                        st_stolen += got;
+                        stat(kStSok, 1);
+                        stat(kStStolen, got);
                     }
                     n = got;
                     qc = vqq;
                 } else if (lane == 0) {
-                    ++st_sfail;
+                    stat(kStSfail, 1);
                 }
             }
         }
         done_seen = __shfl_sync(0xffffffffu, done_seen, 31);
         if (n == 0) {
             // idle: termination check + watchdog + backoff
-            if (lane == 0) ++st_idle;
+            if (lane == 0) stat(kStIdle, 1);
             uint32_t d = 0;
             if (lane == 0) d = ld_relaxed(&p.ctl->done);
             d = __shfl_sync(0xffffffffu, d, 0);
@@ -384,7 +405,7 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
             continue;
         }
         backoff = 32;
-        if (lane == 0) { ++st_cyc; st_inv += n; }
+        if (lane == 0) { stat(kStCyc, 1); stat(kStInv, n); }
 
         // ================= (2) execute, one task per lane =================
         Out o;
@@ -421,7 +442,7 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
                 static_assert(kDataWords == 4, "assist_all takes the 4 request words");
                 if (req) {
                     T::assist_all(args, req, o.ap[0], o.ap[1], o.ap[2], o.ap[3], lane, bx);
-                    if (lane == 0) st_assist += (uint32_t)__popc(req);
+                    if (lane == 0) stat(kStAssist, (uint32_t)__popc(req));
                     req = 0u;
                 }
             }
@@ -434,7 +455,7 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
                 const bool aok = T::assist(args, ap, lane, bx);
                 const uint32_t okm = __ballot_sync(0xffffffffu, aok);
                 if (lane == src && okm != 0xffffffffu) o.err = GTAP_E_BAD_STATE;
-                if (lane == 0) ++st_assist;
+                if (lane == 0) stat(kStAssist, 1);
             }
             if (any_assist) {
                 __threadfence();
@@ -495,7 +516,7 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
         }
         __syncwarp();
         if (failed) break;
-        if (lane == 0) st_tasks += T_total;
+        if (lane == 0) stat(kStTasks, T_total);
 
         // ================= (3b) spawn: write child records =================
         uint32_t cid[MAXC];
@@ -579,7 +600,7 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
                 st_relaxed(&p.fring[((size_t)home << p.logM) + (slot & mmask)], fid + 1u);
             }
             const uint32_t rf = __ballot_sync(0xffffffffu, remote);
-            if (lane == 0) st_rfree += __popc(rf);
+            if (lane == 0) stat(kStRfree, (uint32_t)__popc(rf));
         }
         __syncwarp();
         if (fin && err == 0u) {
@@ -734,7 +755,7 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
 #pragma unroll
         for (int q = 0; q < NQ; ++q) tail[q] += pushq[q];
         nkept = keep;
-        if (lane == 0) st_push += pushc;
+        if (lane == 0) stat(kStPush, pushc);
         // publish the oldest half of a private part when thieves drained its public part,
         // or all of it when heavy tasks were just pushed there
 #pragma unroll
@@ -764,18 +785,18 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
     // ---- exit: fold per-warp counters into the control block
     if (lane == 0) {
         unsigned long long* s = p.ctl->stats;
-        atomicAdd(&s[ST_TASKS], st_tasks);
-        atomicAdd(&s[ST_INVOC], st_inv);
-        atomicAdd(&s[ST_POPS], st_pops);
-        atomicAdd(&s[ST_KEPT], st_kept);
-        atomicAdd(&s[ST_STEALS_OK], st_sok);
-        atomicAdd(&s[ST_STEALS_FAILED], st_sfail);
-        atomicAdd(&s[ST_STOLEN], st_stolen);
-        atomicAdd(&s[ST_PUSHES], st_push);
-        atomicAdd(&s[ST_CYCLES], st_cyc);
-        atomicAdd(&s[ST_IDLE], st_idle);
-        atomicAdd(&s[ST_REMOTE_FREES], st_rfree);
-        if (st_assist) atomicAdd(&s[ST_ASSISTS], st_assist);
+        atomicAdd(&s[ST_TASKS], stget(kStTasks));
+        atomicAdd(&s[ST_INVOC], stget(kStInv));
+        atomicAdd(&s[ST_POPS], stget(kStPops));
+        atomicAdd(&s[ST_KEPT], stget(kStKept));
+        atomicAdd(&s[ST_STEALS_OK], stget(kStSok));
+        atomicAdd(&s[ST_STEALS_FAILED], stget(kStSfail));
+        atomicAdd(&s[ST_STOLEN], stget(kStStolen));
+        atomicAdd(&s[ST_PUSHES], stget(kStPush));
+        atomicAdd(&s[ST_CYCLES], stget(kStCyc));
+        atomicAdd(&s[ST_IDLE], stget(kStIdle));
+        atomicAdd(&s[ST_REMOTE_FREES], stget(kStRfree));
+        if (stget(kStAssist)) atomicAdd(&s[ST_ASSISTS], stget(kStAssist));
         atomicMax(&s[ST_MAX_POOL], (unsigned long long)bump);
     }
 }

@@ -932,6 +932,7 @@ struct MergesortTable {
     static constexpr int kMaxThreads = 128;                    // __launch_bounds__
     static constexpr int kMinBlocks = MODE == 1u ? GTAP_MS_WARP_MINB : 4;
     static constexpr bool kAssist = MODE == 1u;                // leaf and merge bodies: warp assist
+    static constexpr bool kStatsSmem = true;   // scheduler statistics in smem: frees 24 registers (no spills at 128)
     static constexpr int kFreeStack = 0;   // own free stack off: measured 2-3 % slower here (few live records, smem-heavy blocks)
 #ifndef GTAP_MS_ASSIST_MIN
 #define GTAP_MS_ASSIST_MIN 0

@@ -1,0 +1,91 @@
+"""GPU parity of the build options that are off (or sized) by default in the product library.
+
+Each variant library is compiled here (paper_2604_05982_b200/build.py with -D defines, the same
+nvcc sm_100a flags) and exercised in a subprocess with GTAP_LIB pointing at it, against the
+oracle: the options are alternative implementations of the same task bodies / scheduler paths
+(DESIGN.md §5 "Measured and rejected", the own free stack), so every result must stay bit-exact.
+
+* GTAP_FSTACK=1, GTAP_FIB_FSTACK=1: a one-entry own free stack, so nearly every surplus free takes
+  the overflow path to the home free ring (fib, trees, Cilksort, N-Queens).
+* GTAP_MS_TILE_BITONIC=0 / 2: the merge-path-search tile bodies of the warp merge.
+* GTAP_MS_GUIDED=1, GTAP_MS_BATCH=1, GTAP_LEAF_LANE_MAJOR=1: guided chunks on the GPU-wide board,
+  batched leaf / small-merge assists, lane-major leaf sort.
+"""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+# runs in the subprocess: prints one JSON object of checks
+_PROBE = r"""
+import json, sys
+import numpy as np
+import torch
+sys.path.insert(0, %(root)r)
+import oracle, synth
+import paper_2604_05982_b200 as g
+res = {}
+what = %(what)r
+cfg = dict(grid_size=148, block_size=128, max_tasks_per_worker=4096, watchdog_ns=60_000_000_000)
+if "fib" in what:
+    for n in (0, 1, 2, 20, 25):
+        v, st = g.fib(n, **cfg)
+        ov, ot, oi = oracle.fib(n)
+        res[f"fib{n}"] = (v, st.tasks, st.invocations) == (ov, ot, oi)
+if "tree" in what:
+    buf_cpu = synth.tree_buffer(1 << 14)
+    buf = buf_cpu.to("cuda")
+    for pruned, D in ((False, 12), (True, 14)):
+        v, st = g.tree(D, buf, 4, 8, pruned=pruned, **cfg)
+        res[f"tree{int(pruned)}"] = (v, st.tasks) == oracle.tree(D, buf_cpu.numpy().view(np.uint64), 4, 8, pruned=pruned)
+if "nq" in what:
+    c, st = g.nqueens(10, 4, **cfg)
+    res["nq10"] = (int(c), st.tasks) == oracle.nqueens(10, 4)
+for name, n in (("ms", 1 << 18), ("ms_ragged", 100003), ("ms_big", 1 << 22)):
+    if "ms" not in what:
+        break
+    keys = synth.keys_int32(n, seed=n).numpy()
+    d = torch.from_numpy(keys).cuda()
+    st = g.mergesort_(d, cutoff=128, merge_mode=1, grid_size=148 * 4, block_size=128, max_tasks_per_worker=1024,
+                      watchdog_ns=60_000_000_000)
+    ref, tasks, inv = oracle.mergesort(keys, 128)
+    res[name] = bool(np.array_equal(d.cpu().numpy(), ref)) and st.tasks == tasks
+if "cs" in what:
+    keys = synth.keys_int32(300007, seed=5).numpy()
+    d = torch.from_numpy(keys).cuda()
+    st = g.cilksort_(d, None, 64, 256, **cfg)
+    ref = oracle.cilksort(keys, 64, 256)
+    res["cs"] = bool(np.array_equal(d.cpu().numpy(), ref[0])) and st.tasks == ref[1]
+print(json.dumps(res))
+"""
+
+
+def _variant(defines):
+    sys.path.insert(0, ROOT)
+    from paper_2604_05982_b200 import build as b
+    return b.build(defines=defines)
+
+
+def _probe(lib, what):
+    env = dict(os.environ, GTAP_LIB=lib)
+    code = _PROBE % {"root": ROOT, "what": what}
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    return json.loads(r.stdout.strip().splitlines()[-1])
+
+
+@pytest.mark.parametrize("defines,what", [
+    (("GTAP_FSTACK=1", "GTAP_FIB_FSTACK=1"), "fib tree nq cs"),
+    (("GTAP_MS_TILE_BITONIC=0",), "ms"),
+    (("GTAP_MS_TILE_BITONIC=2",), "ms"),
+    (("GTAP_MS_GUIDED=1", "GTAP_MS_GUIDED_MIN=16384", "GTAP_MS_BATCH=1", "GTAP_LEAF_LANE_MAJOR=1"), "ms"),
+], ids=["fstack1", "tile_search", "tile_search_inreg", "guided_batch_lanemajor"])
+def test_variant_parity(cuda_device, defines, what):
+    lib = _variant(defines)
+    res = _probe(lib, what)
+    assert res and all(res.values()), res

@@ -29,6 +29,10 @@ struct BfsTable {
 #define GTAP_BFS_U 4
 #endif
     static constexpr uint32_t kU = GTAP_BFS_U;       // edges per thread per step
+#ifndef GTAP_BFS_POP_BATCH
+#define GTAP_BFS_POP_BATCH 4
+#endif
+    static constexpr int kPopBatch = GTAP_BFS_POP_BATCH;  // sched_block.cuh batch pop
     struct Scratch {
         uint32_t unused;
     };

@@ -10,6 +10,7 @@ oracle: the options are alternative implementations of the same task bodies / sc
 * GTAP_MS_TILE_BITONIC=0 / 2: the merge-path-search tile bodies of the warp merge.
 * GTAP_MS_GUIDED=1, GTAP_MS_BATCH=1, GTAP_LEAF_LANE_MAJOR=1: guided chunks on the GPU-wide board,
   batched leaf / small-merge assists, lane-major leaf sort.
+* GTAP_BFS_POP_BATCH=0 / 32: single pops and the largest batch pop of the block-level leader.
 """
 import json
 import os
@@ -55,6 +56,13 @@ for name, n in (("ms", 1 << 18), ("ms_ragged", 100003), ("ms_big", 1 << 22)):
                       watchdog_ns=60_000_000_000)
     ref, tasks, inv = oracle.mergesort(keys, 128)
     res[name] = bool(np.array_equal(d.cpu().numpy(), ref)) and st.tasks == tasks
+if "bfs" in what:
+    rp, col = synth.rmat_csr(14, 16, seed=4)
+    src = synth.bfs_sources(rp, 1, seed=4)[0]
+    for grid, block in ((148, 64), (1, 32)):
+        depth, st = g.bfs(rp.cuda(), col.cuda(), src, grid_size=grid, block_size=block, max_tasks_per_worker=1 << 16,
+                          steal_max=32, watchdog_ns=60_000_000_000)
+        res[f"bfs{grid}"] = bool(np.array_equal(depth.cpu().numpy(), oracle.bfs(rp, col, src)))
 if "cs" in what:
     keys = synth.keys_int32(300007, seed=5).numpy()
     d = torch.from_numpy(keys).cuda()
@@ -84,7 +92,9 @@ def _probe(lib, what):
     (("GTAP_MS_TILE_BITONIC=0",), "ms"),
     (("GTAP_MS_TILE_BITONIC=2",), "ms"),
     (("GTAP_MS_GUIDED=1", "GTAP_MS_GUIDED_MIN=16384", "GTAP_MS_BATCH=1", "GTAP_LEAF_LANE_MAJOR=1"), "ms"),
-], ids=["fstack1", "tile_search", "tile_search_inreg", "guided_batch_lanemajor"])
+    (("GTAP_BFS_POP_BATCH=0",), "bfs"),
+    (("GTAP_BFS_POP_BATCH=32",), "bfs"),
+], ids=["fstack1", "tile_search", "tile_search_inreg", "guided_batch_lanemajor", "bfs_pop1", "bfs_pop32"])
 def test_variant_parity(cuda_device, defines, what):
     lib = _variant(defines)
     res = _probe(lib, what)

@@ -10,6 +10,7 @@ oracle: the options are alternative implementations of the same task bodies / sc
 * GTAP_MS_TILE_BITONIC=0 / 2: the merge-path-search tile bodies of the warp merge.
 * GTAP_MS_GUIDED=1, GTAP_MS_BATCH=1, GTAP_LEAF_LANE_MAJOR=1: guided chunks on the GPU-wide board,
   batched leaf / small-merge assists, lane-major leaf sort.
+* GTAP_CS_KARY=0: Cilksort's plain binary split search.
 * GTAP_BFS_POP_BATCH=0 / 32: single pops and the largest batch pop of the block-level leader.
 """
 import json
@@ -92,9 +93,11 @@ def _probe(lib, what):
     (("GTAP_MS_TILE_BITONIC=0",), "ms"),
     (("GTAP_MS_TILE_BITONIC=2",), "ms"),
     (("GTAP_MS_GUIDED=1", "GTAP_MS_GUIDED_MIN=16384", "GTAP_MS_BATCH=1", "GTAP_LEAF_LANE_MAJOR=1"), "ms"),
+    (("GTAP_CS_KARY=0",), "cs"),
     (("GTAP_BFS_POP_BATCH=0",), "bfs"),
     (("GTAP_BFS_POP_BATCH=32",), "bfs"),
-], ids=["fstack1", "tile_search", "tile_search_inreg", "guided_batch_lanemajor", "bfs_pop1", "bfs_pop32"])
+], ids=["fstack1", "tile_search", "tile_search_inreg", "guided_batch_lanemajor", "cs_binary_split", "bfs_pop1",
+        "bfs_pop32"])
 def test_variant_parity(cuda_device, defines, what):
     lib = _variant(defines)
     res = _probe(lib, what)

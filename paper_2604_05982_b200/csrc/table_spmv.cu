@@ -81,16 +81,26 @@ struct SpmvTable {
             const uint32_t k = d[0], R = d[1], r0 = d[2], r1 = d[3] ? d[3] : a.nrows;
             const long long s0 = __ldg(&a.row_ptr[r0]);
             const unsigned long long nnz = (unsigned long long)(__ldg(&a.row_ptr[r1]) - s0);
+            // block-parallel search: every thread probes one of blockDim points per round and
+            // __syncthreads_count ranks the boundary (~log_{blockDim+1}(rows) round trips instead of
+            // the ~22 of a binary search, twice per root at the start of the run)
+            const uint32_t bdim = blockDim.x, tix = threadIdx.x;
             auto bound = [&](uint32_t j) -> uint32_t {
                 if (j == 0u) return r0;
                 if (j >= R) return r1;
                 const long long target = s0 + (long long)((nnz * j) / R);
-                uint32_t l = r0, h = r1;
-                while (l < h) {
-                    const uint32_t mid = (l + h) >> 1;
-                    if ((long long)__ldg(&a.row_ptr[mid]) < target) l = mid + 1u; else h = mid;
+                uint32_t l = r0, h = r1;   // smallest i in [l, h] with row_ptr[i] >= target
+                while (h - l > bdim) {
+                    const unsigned long long w = h - l;
+                    const uint32_t q = l + (uint32_t)(((unsigned long long)(tix + 1u) * w) / (bdim + 1u));
+                    const uint32_t cnt = (uint32_t)__syncthreads_count((long long)__ldg(&a.row_ptr[q]) < target);
+                    const uint32_t nl = cnt == 0u ? l : l + (uint32_t)(((unsigned long long)cnt * w) / (bdim + 1u)) + 1u;
+                    const uint32_t nh = cnt == bdim ? h : l + (uint32_t)(((unsigned long long)(cnt + 1u) * w) / (bdim + 1u));
+                    l = nl;
+                    h = nh;
                 }
-                return l;
+                const uint32_t q = l + tix;
+                return l + (uint32_t)__syncthreads_count(q < h && (long long)__ldg(&a.row_ptr[q]) < target);
             };
             lo = bound(k);
             hi = max(lo, bound(k + 1u));

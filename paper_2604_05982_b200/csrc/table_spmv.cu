@@ -40,7 +40,10 @@ struct SpmvTable {
 #ifndef GTAP_SPMV_ROWS_BY_THREAD
 #define GTAP_SPMV_ROWS_BY_THREAD 1
 #endif
-    static constexpr int kShortSeg = 64;    // in-chunk row segments up to this long: one thread
+#ifndef GTAP_SPMV_SHORT
+#define GTAP_SPMV_SHORT 64
+#endif
+    static constexpr int kShortSeg = GTAP_SPMV_SHORT;    // in-chunk row segments up to this long: one thread
     static constexpr int kLongCap = kPer * kMaxBlock / (kShortSeg + 1) + 1;  // > segments that fit a chunk
     struct Scratch {
         float prod[kPer * kMaxBlock];

@@ -154,6 +154,10 @@ inline size_t reset_span_front(const Layout& L) { return L.roots; }
 
 #ifndef GTAP_HOST_ONLY
 namespace gtap {
+// zero `bytes` of device memory on `s` with an SM kernel (runtime.cu; no copy engine, so it never
+// queues behind a user's bulk copies); falls back to cudaMemsetAsync for unaligned ranges
+cudaError_t zero_async(void* p, size_t bytes, cudaStream_t s);
+
 namespace dev {
 
 // ---- strong (L1-bypassing, L2-coherent) accesses ---------------------------

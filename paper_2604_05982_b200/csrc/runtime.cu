@@ -33,8 +33,10 @@ struct gtap_runtime {
     bool owns_ws;
     std::vector<RootSpec> roots;
     const gtap_task_table* table;
-    RootSpec* h_roots;     // pinned staging (max_roots)
-    Ctl* h_ctl;            // pinned: control block staging / readback
+    RootSpec* h_roots;     // pinned, mapped: root staging (max_roots)
+    Ctl* h_ctl;            // pinned, mapped: control block staging / readback
+    RootSpec* dh_roots;    // device aliases of the two mapped buffers
+    Ctl* dh_ctl;
     cudaEvent_t ev0, ev1, ev2;   // kernel start / end, control-block readback done
     bool in_flight;
     bool dirty;            // workspace used since the last reset
@@ -113,13 +115,46 @@ gtap_status geometry(gtap_runtime* rt, const gtap_task_table* t, uint32_t* W, ui
     return GTAP_OK;
 }
 
+// Small transfers and fills by SM kernels instead of cudaMemcpyAsync / cudaMemsetAsync: a run's
+// root / control-block staging and readback then never queue behind a user's bulk copy on the
+// same copy engine (the bench's pipelined e2e overlaps 64 MB H2D and D2H copies with the sort; the
+// 200-byte control-block readback waited ~1 ms behind them before each gtap_sync returned).
+__global__ void word_copy_kernel(const uint32_t* __restrict__ s0, uint32_t* __restrict__ d0, uint32_t n0,
+                                 const uint32_t* __restrict__ s1, uint32_t* __restrict__ d1, uint32_t n1) {
+    for (uint32_t i = threadIdx.x; i < n0; i += blockDim.x) d0[i] = s0[i];
+    for (uint32_t i = threadIdx.x; i < n1; i += blockDim.x) d1[i] = s1[i];
+}
+__global__ void zero_kernel(uint32_t* __restrict__ p, size_t words) {
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    uint4* p4 = reinterpret_cast<uint4*>(p);
+    const size_t n4 = words / 4u;
+    for (size_t k = i; k < n4; k += stride) p4[k] = make_uint4(0u, 0u, 0u, 0u);
+    for (size_t k = n4 * 4u + i; k < words; k += stride) p[k] = 0u;
+}
+
+}  // namespace
+
+namespace gtap {
+cudaError_t zero_async(void* p, size_t bytes, cudaStream_t s) {
+    if (bytes == 0) return cudaSuccess;
+    if ((bytes & 3u) || ((uintptr_t)p & 15u)) return cudaMemsetAsync(p, 0, bytes, s);
+    const size_t words = bytes / 4u;
+    const unsigned blocks = (unsigned)std::min<size_t>((words / 4u + 255u) / 256u + 1u, 148u * 8u);
+    zero_kernel<<<blocks, 256, 0, s>>>(static_cast<uint32_t*>(p), words);
+    return cudaGetLastError();
+}
+}  // namespace gtap
+
+namespace {
+
 gtap_status do_reset(gtap_runtime* rt, cudaStream_t s) {
     cudaSetDevice(rt->device);
     const Layout& L = rt->L;
     // control block, deque metadata, free-ring metadata (contiguous at the front)
-    if (cudaMemsetAsync(rt->ws + L.ctl, 0, L.roots - L.ctl, s) != cudaSuccess) return GTAP_E_CUDA;
+    if (gtap::zero_async(rt->ws + L.ctl, L.roots - L.ctl, s) != cudaSuccess) return GTAP_E_CUDA;
     // free rings: entry 0 = empty
-    if (cudaMemsetAsync(rt->ws + L.fring, 0, sizeof(uint32_t) * (size_t)L.W * L.M, s) != cudaSuccess)
+    if (gtap::zero_async(rt->ws + L.fring, sizeof(uint32_t) * (size_t)L.W * L.M, s) != cudaSuccess)
         return GTAP_E_CUDA;
     rt->dirty = false;
     return GTAP_OK;
@@ -205,8 +240,10 @@ gtap_status gtap_init(const gtap_config* in, void* d_workspace, size_t bytes, gt
         if (cudaMalloc(&rt->ws, rt->L.total) != cudaSuccess) { delete rt; return GTAP_E_NOMEM; }
         rt->owns_ws = true;
     }
-    if (cudaHostAlloc(&rt->h_roots, sizeof(RootSpec) * rt->max_roots, cudaHostAllocDefault) != cudaSuccess ||
-        cudaHostAlloc(&rt->h_ctl, sizeof(Ctl), cudaHostAllocDefault) != cudaSuccess) {
+    if (cudaHostAlloc(&rt->h_roots, sizeof(RootSpec) * rt->max_roots, cudaHostAllocMapped) != cudaSuccess ||
+        cudaHostAlloc(&rt->h_ctl, sizeof(Ctl), cudaHostAllocMapped) != cudaSuccess ||
+        cudaHostGetDevicePointer(reinterpret_cast<void**>(&rt->dh_roots), rt->h_roots, 0) != cudaSuccess ||
+        cudaHostGetDevicePointer(reinterpret_cast<void**>(&rt->dh_ctl), rt->h_ctl, 0) != cudaSuccess) {
         gtap_finalize(rt);
         return GTAP_E_NOMEM;
     }
@@ -275,14 +312,16 @@ gtap_status gtap_run(gtap_runtime* rt, void* stream) {
     const uint32_t nroots = (uint32_t)rt->roots.size();
     // roots + termination counters: one pinned H2D copy each
     std::memcpy(rt->h_roots, rt->roots.data(), sizeof(RootSpec) * nroots);
-    if (cudaMemcpyAsync(rt->ws + rt->L.roots, rt->h_roots, sizeof(RootSpec) * nroots, cudaMemcpyHostToDevice, s) !=
-        cudaSuccess)
-        return GTAP_E_CUDA;
     std::memset(rt->h_ctl, 0, sizeof(Ctl));
     rt->h_ctl->roots_left = nroots;
     rt->h_ctl->outstanding = nroots;
-    if (cudaMemcpyAsync(rt->ws + rt->L.ctl, rt->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, s) != cudaSuccess)
-        return GTAP_E_CUDA;
+    // one SM kernel reads both from the mapped host buffers (no copy engine, see word_copy_kernel)
+    static_assert(sizeof(RootSpec) % 4 == 0 && sizeof(Ctl) % 4 == 0, "word copies");
+    word_copy_kernel<<<1, 256, 0, s>>>(reinterpret_cast<const uint32_t*>(rt->dh_roots),
+                                       reinterpret_cast<uint32_t*>(rt->ws + rt->L.roots),
+                                       (uint32_t)(sizeof(RootSpec) * nroots / 4), reinterpret_cast<const uint32_t*>(rt->dh_ctl),
+                                       reinterpret_cast<uint32_t*>(rt->ws + rt->L.ctl), (uint32_t)(sizeof(Ctl) / 4));
+    if (cudaGetLastError() != cudaSuccess) return GTAP_E_CUDA;
 
     KParams p{};
     p.W = W;
@@ -312,9 +351,10 @@ gtap_status gtap_run(gtap_runtime* rt, void* stream) {
     if (cudaEventRecord(rt->ev1, s) != cudaSuccess) return GTAP_E_CUDA;
     // the control block (error word, counters) comes back on the same stream right behind the kernel,
     // so gtap_sync waits for this run only (no legacy-stream synchronous copy)
-    if (cudaMemcpyAsync(rt->h_ctl, rt->ws + rt->L.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-        cudaEventRecord(rt->ev2, s) != cudaSuccess)
-        return GTAP_E_CUDA;
+    word_copy_kernel<<<1, 256, 0, s>>>(reinterpret_cast<const uint32_t*>(rt->ws + rt->L.ctl),
+                                       reinterpret_cast<uint32_t*>(rt->dh_ctl), (uint32_t)(sizeof(Ctl) / 4), nullptr,
+                                       nullptr, 0u);
+    if (cudaGetLastError() != cudaSuccess || cudaEventRecord(rt->ev2, s) != cudaSuccess) return GTAP_E_CUDA;
     rt->in_flight = true;
     rt->dirty = true;
     rt->run_grid = grid;

@@ -1384,7 +1384,7 @@ extern "C" const gtap_task_table* gtap_table_mergesort_ex(int32_t* keys, int32_t
     if (gb) {
         t->dev_scratch = gb;
         t->prepare = [](const gtap_task_table* tt, cudaStream_t s) {
-            return cudaMemsetAsync(tt->dev_scratch, 0, sizeof(gtap::GBoard), s);
+            return gtap::zero_async(tt->dev_scratch, sizeof(gtap::GBoard), s);
         };
     }
     return t;

@@ -1,6 +1,10 @@
 // warp_merge_micro.cu -- time the warp-assist merge (warp_merge) in isolation: one warp (or W
 // warps on W separate problems), two sorted runs of n/2 keys; checks the output.
 #include "../paper_2604_05982_b200/csrc/table_mergesort.cu"
+// the table's board reset calls the runtime's fill helper (runtime.cu, not linked here)
+namespace gtap {
+cudaError_t zero_async(void* p, size_t bytes, cudaStream_t s) { return cudaMemsetAsync(p, 0, bytes, s); }
+}  // namespace gtap
 #include <algorithm>
 #include <cstdio>
 #include <vector>

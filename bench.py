@@ -348,6 +348,27 @@ def bench_fib(dev, reps=3):
                 join_atomics=tasks - 1)
 
 
+def bench_fib20(dev, reps=20):
+    """BASELINE configs[0] / SURVEY §8(d) C1: fib(20) (21,891 tasks) is span-bound -- its critical path is
+    2n - 1 = 39 dependent invocations -- so it is reported as tasks/s and as time per critical-path step."""
+    import paper_2604_05982_b200 as g
+    rt = g.Runtime(g.GTAP_WORKER_THREAD, dev.index, **FIB_CFG)
+    ms = []
+    st = None
+    for i in range(reps + 1):
+        v, st = g.fib(20, rt=rt)
+        assert v == 6765
+        if i:
+            ms.append(st.device_ms)
+    rt.close()
+    t = statistics.median(ms)
+    return dict(workload="fib(20) no cutoff, thread-level (configs[0]), launch + span bound", metric="tasks/s",
+                value=st.tasks / (t * 1e-3), ms=t, tasks=st.tasks, invocations=st.invocations,
+                us_per_critical_path_invocation=t * 1e3 / 39.0,
+                note="critical path 2n-1 = 39 dependent invocations (SURVEY §8(a) A12a); includes the persistent "
+                     "kernel's start and drain")
+
+
 def bench_epaq(dev, cutoff=10, reps=3):
     """SURVEY §8(f) NEXT #1: fib(40) with cutoff 10, 1 queue vs EPAQ with 3 queues (P:788-789)."""
     import paper_2604_05982_b200 as g
@@ -527,7 +548,7 @@ def bench_spmv(dev, ws=1, rank=0, reps=5):
                 traffic=profile_traffic("spmv"), scaling="strong", y_checksum=float(y.double().sum().item()))
 
 
-def bench_bfs(dev, nsrc=4):
+def bench_bfs(dev, nsrc=4, ws=1, rank=0):
     import torch
 
     import synth
@@ -535,7 +556,10 @@ def bench_bfs(dev, nsrc=4):
     rp, col = synth.rmat_csr(BFS_SCALE, 16, seed=3, device=dev)
     depth = torch.empty(rp.numel() - 1, dtype=torch.int32, device=dev)
     rt = g.Runtime(g.GTAP_WORKER_BLOCK, dev.index, **BFS_CFG)
-    srcs = synth.bfs_sources(rp, nsrc + 1, seed=5)
+    # multi-GPU: the graph is replicated and the sources are split over the ranks; source 0
+    # of every rank's list is a warm-up
+    allsrc = synth.bfs_sources(rp, nsrc * ws, seed=5)
+    srcs = [allsrc[rank * nsrc]] + allsrc[rank * nsrc: (rank + 1) * nsrc]
     res = []
     for i, s in enumerate(srcs):
         rt.reset()
@@ -548,9 +572,19 @@ def bench_bfs(dev, nsrc=4):
         res.append((edges / (st.device_ms * 1e-3), st.device_ms, st.tasks, int(reached.sum().item())))
     rt.close()
     teps = statistics.median(r[0] for r in res)
-    return dict(workload="BFS RMAT scale 22 ef 16 (configs[4]), block-level", metric="GTEPS", value=teps / 1e9,
-                ms=statistics.median(r[1] for r in res), tasks=[r[2] for r in res], reached=[r[3] for r in res],
-                sources=len(res))
+    out = dict(workload="BFS RMAT scale 22 ef 16 (configs[4]), block-level", metric="GTEPS", value=teps / 1e9,
+               ms=statistics.median(r[1] for r in res), tasks=[r[2] for r in res], reached=[r[3] for r in res],
+               sources=len(res))
+    if ws > 1:  # aggregate: every rank's edges over the slowest rank's total time (no collective on the path)
+        import torch.distributed as dist
+        t = torch.tensor([sum(r[1] for r in res), sum(r[0] * r[1] * 1e-3 for r in res)], dtype=torch.float64,
+                         device=dev)
+        allv = [torch.zeros_like(t) for _ in range(ws)]
+        dist.all_gather(allv, t)
+        tmax = max(float(v[0]) for v in allv)
+        edges = sum(float(v[1]) for v in allv)
+        out.update(aggregate_gteps=edges / (tmax * 1e-3) / 1e9, sources_total=nsrc * ws, scaling="weak")
+    return out
 
 
 def cpu_baseline(sample_n=1 << 22, budget_s=12.0):
@@ -592,6 +626,7 @@ def run_ours(args):
                                     peak_source="measured live: gtap_ubench_atomics kind 5 (atom.acq_rel.add, "
                                                 "distinct L2-resident sectors)")
             secondary.append(fibr)
+            secondary.append(bench_fib20(dev))
             secondary.append(dict(workload="L2 atomic probes", metric="ops/s", value=atoms))
             secondary.append(bench_epaq(dev))
             secondary.append(bench_nqueens(dev))
@@ -606,7 +641,7 @@ def run_ours(args):
         except Exception as e:
             secondary.append(dict(workload="bench_spmv", error=repr(e)))
         try:
-            secondary.append(bench_bfs(dev))
+            secondary.append(bench_bfs(dev, ws=ws, rank=rank))
         except Exception as e:
             secondary.append(dict(workload="bench_bfs", error=repr(e)))
     # the only collective: gather per-rank checksums after timing

@@ -823,8 +823,14 @@ __device__ __noinline__ uint2 warp_split2(const int32_t* src, uint32_t l, uint32
                       lo1 + (uint32_t)__popc(__ballot_sync(0xffffffffu, a1)));
 }
 
-constexpr uint32_t kBlockAssistMin = 1u << 17;  // merges this long are shared by the block's warps
-constexpr uint32_t kChunk = 1u << 16;           // output keys per claimed chunk
+#ifndef GTAP_MS_BLOCK_MIN
+#define GTAP_MS_BLOCK_MIN (1u << 17)
+#endif
+#ifndef GTAP_MS_BCHUNK
+#define GTAP_MS_BCHUNK (1u << 16)
+#endif
+constexpr uint32_t kBlockAssistMin = GTAP_MS_BLOCK_MIN;  // merges this long are shared by the block's warps
+constexpr uint32_t kChunk = GTAP_MS_BCHUNK;      // output keys per claimed chunk (block board)
 
 // GPU-wide assist board (GTAP_MERGE_WARP, merges >= kGlobalAssistMin): any idle warp of the grid
 // claims kGChunk-key output chunks of an open slot. Slot protocol (all words in global memory):

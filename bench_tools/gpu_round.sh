@@ -15,3 +15,6 @@ timeout -s KILL 600 ncu --set full --import-source on --clock-control none -k re
     -o gpurun_out/${R}_prof_spmv --force-overwrite python bench_tools/profile_one.py spmv 0 2 > /dev/null 2>&1; echo "ncu spmv rc=$?"
 timeout -s KILL 600 ncu --set full --import-source on --clock-control none -k regex:thread_sched -s 1 -c 1 \
     -o gpurun_out/${R}_prof_fib --force-overwrite python bench_tools/profile_one.py fib 40 2 > /dev/null 2>&1; echo "ncu fib rc=$?"
+timeout -s KILL 600 ncu --set full --import-source on --clock-control none -k regex:block_sched -s 1 -c 1 \
+    -o gpurun_out/${R}_prof_bfs --force-overwrite python bench_tools/profile_one.py bfs 22 2 > /dev/null 2>&1; echo "ncu bfs rc=$?"
+timeout -s KILL 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')"

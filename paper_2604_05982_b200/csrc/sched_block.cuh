@@ -28,6 +28,11 @@ namespace gtap {
 // single pops would. Tables without kPopBatch pop one task at a time (measured: SpMV and the
 // block-level trees are slower with batches, BFS faster with 4).
 template <class T, class = void>
+struct pop_oldest_of { static constexpr bool value = false; };
+template <class T>
+struct pop_oldest_of<T, decltype((void)T::kPopOldest, void())> { static constexpr bool value = T::kPopOldest; };
+
+template <class T, class = void>
 struct pop_batch_of { static constexpr int value = 0; };
 template <class T>
 struct pop_batch_of<T, decltype((void)T::kPopBatch, void())> { static constexpr int value = T::kPopBatch; };
@@ -307,7 +312,16 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) block_sched_ker
             } else if (kPB > 1 && L.tail - L.split >= 2u) {   // batch pop, private part
                 const uint32_t c = min((uint32_t)kPB, (L.tail - L.split) >> 1);
                 if (lane < c) {
-                    const uint32_t bid = ld_relaxed(&ring[(L.tail - 1u - lane) & qmask]);
+                    uint32_t bid;
+                    if constexpr (pop_oldest_of<T>::value) {
+                        // the c OLDEST private tasks (bottom of the private part); the c newest move into
+                        // their slots (c <= half the private part: no overlap; thieves never read past split)
+                        bid = ld_relaxed(&ring[(L.split + lane) & qmask]);
+                        const uint32_t top = ld_relaxed(&ring[(L.tail - 1u - lane) & qmask]);
+                        ring[(L.split + lane) & qmask] = top;
+                    } else {
+                        bid = ld_relaxed(&ring[(L.tail - 1u - lane) & qmask]);
+                    }
                     sm.bq_id[lane] = bid;
                     sm.bq_h[lane] = ld_relaxed_v4(p.rec + bid);
                     sm.bq_d[lane] = ld_relaxed_v4(&p.rec[bid].d[0]);

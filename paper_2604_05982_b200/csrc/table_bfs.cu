@@ -33,6 +33,11 @@ struct BfsTable {
 #define GTAP_BFS_POP_BATCH 4
 #endif
     static constexpr int kPopBatch = GTAP_BFS_POP_BATCH;  // sched_block.cuh batch pop
+#ifndef GTAP_BFS_POP_OLDEST
+#define GTAP_BFS_POP_OLDEST 1
+#endif
+    // batch pops take the oldest private tasks (closer to level order: fewer re-expansions)
+    static constexpr bool kPopOldest = GTAP_BFS_POP_OLDEST != 0;
     struct Scratch {
         uint32_t unused;
     };

@@ -11,7 +11,8 @@ oracle: the options are alternative implementations of the same task bodies / sc
 * GTAP_MS_GUIDED=1, GTAP_MS_BATCH=1, GTAP_LEAF_LANE_MAJOR=1: guided chunks on the GPU-wide board,
   batched leaf / small-merge assists, lane-major leaf sort.
 * GTAP_CS_KARY=0: Cilksort's plain binary split search.
-* GTAP_BFS_POP_BATCH=0 / 32: single pops and the largest batch pop of the block-level leader.
+* GTAP_BFS_POP_BATCH=0 / 32: single pops and the largest batch pop of the block-level leader;
+  GTAP_BFS_POP_OLDEST=0: batch pops from the newest end (LIFO) instead of the oldest private tasks.
 """
 import json
 import os
@@ -96,8 +97,9 @@ def _probe(lib, what):
     (("GTAP_CS_KARY=0",), "cs"),
     (("GTAP_BFS_POP_BATCH=0",), "bfs"),
     (("GTAP_BFS_POP_BATCH=32",), "bfs"),
+    (("GTAP_BFS_POP_OLDEST=0",), "bfs"),
 ], ids=["fstack1", "tile_search", "tile_search_inreg", "guided_batch_lanemajor", "cs_binary_split", "bfs_pop1",
-        "bfs_pop32"])
+        "bfs_pop32", "bfs_pop_newest"])
 def test_variant_parity(cuda_device, defines, what):
     lib = _variant(defines)
     res = _probe(lib, what)

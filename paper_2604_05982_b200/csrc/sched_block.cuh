@@ -27,6 +27,12 @@ namespace gtap {
 // trip per batch instead of per task; the block then runs them one at a time in LIFO order, as
 // single pops would. Tables without kPopBatch pop one task at a time (measured: SpMV and the
 // block-level trees are slower with batches, BFS faster with 4).
+// keep the newest child for the block's next task (default) or push every child (kKeepChild = false)
+template <class T, class = void>
+struct keep_child_of { static constexpr bool value = true; };
+template <class T>
+struct keep_child_of<T, decltype((void)T::kKeepChild, void())> { static constexpr bool value = T::kKeepChild; };
+
 template <class T, class = void>
 struct pop_oldest_of { static constexpr bool value = false; };
 template <class T>
@@ -499,7 +505,8 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) block_sched_ker
             }
             if (ok) {
                 // a resumed parent takes the kept slot later; the kept child is then pushed
-                ok = block_publish_spawns<T>(p, L, sm, w, lane, staged, T::kTaskwait ? my : kNone, true, false);
+                ok = block_publish_spawns<T>(p, L, sm, w, lane, staged, T::kTaskwait ? my : kNone, keep_child_of<T>::value,
+                                             false);
             }
             if (ok) {
                 if (sm.action == 2) {

@@ -38,6 +38,10 @@ struct BfsTable {
 #endif
     // batch pops take the oldest private tasks (closer to level order: fewer re-expansions)
     static constexpr bool kPopOldest = GTAP_BFS_POP_OLDEST != 0;
+#ifndef GTAP_BFS_KEEP_CHILD
+#define GTAP_BFS_KEEP_CHILD 0   // every child to the deque (oldest-first batch pops): 8.3-8.6 -> 8.1-8.2 ms median
+#endif
+    static constexpr bool kKeepChild = GTAP_BFS_KEEP_CHILD != 0;
     struct Scratch {
         uint32_t unused;
     };

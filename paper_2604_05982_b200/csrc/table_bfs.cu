@@ -34,12 +34,14 @@ struct BfsTable {
 #endif
     static constexpr int kPopBatch = GTAP_BFS_POP_BATCH;  // sched_block.cuh batch pop
 #ifndef GTAP_BFS_POP_OLDEST
-#define GTAP_BFS_POP_OLDEST 1
+#define GTAP_BFS_POP_OLDEST 0
 #endif
-    // batch pops take the oldest private tasks (closer to level order: fewer re-expansions)
+    // 1: batch pops take the oldest private tasks (closer to level order: 4.83 -> 4.37 M tasks, 8.9 -> 8.4 ms),
+    // but a deque then behaves FIFO and holds a frontier: with small queue capacities (4096 per worker,
+    // RMAT-16) runs hit GTAP_E_QUEUE_OVERFLOW that the LIFO order never reaches, so it is off by default
     static constexpr bool kPopOldest = GTAP_BFS_POP_OLDEST != 0;
 #ifndef GTAP_BFS_KEEP_CHILD
-#define GTAP_BFS_KEEP_CHILD 0   // every child to the deque (oldest-first batch pops): 8.3-8.6 -> 8.1-8.2 ms median
+#define GTAP_BFS_KEEP_CHILD 1   // 0: every child to the deque (8.3-8.6 -> 8.1-8.2 ms with oldest-first pops, but see kPopOldest)
 #endif
     static constexpr bool kKeepChild = GTAP_BFS_KEEP_CHILD != 0;
     struct Scratch {

@@ -12,8 +12,8 @@ oracle: the options are alternative implementations of the same task bodies / sc
   batched leaf / small-merge assists, lane-major leaf sort.
 * GTAP_CS_KARY=0: Cilksort's plain binary split search.
 * GTAP_BFS_POP_BATCH=0 / 32: single pops and the largest batch pop of the block-level leader;
-  GTAP_BFS_POP_OLDEST=0: batch pops from the newest end (LIFO) instead of the oldest private tasks;
-  GTAP_BFS_KEEP_CHILD=1: the block keeps its newest child for its next task.
+  GTAP_BFS_POP_OLDEST=1 (+ GTAP_BFS_KEEP_CHILD=0): batch pops of the oldest private tasks, with every
+  child pushed instead of the newest kept for the block's next task.
 """
 import json
 import os
@@ -98,10 +98,10 @@ def _probe(lib, what):
     (("GTAP_CS_KARY=0",), "cs"),
     (("GTAP_BFS_POP_BATCH=0",), "bfs"),
     (("GTAP_BFS_POP_BATCH=32",), "bfs"),
-    (("GTAP_BFS_POP_OLDEST=0",), "bfs"),
-    (("GTAP_BFS_KEEP_CHILD=1",), "bfs"),
+    (("GTAP_BFS_POP_OLDEST=1",), "bfs"),
+    (("GTAP_BFS_POP_OLDEST=1", "GTAP_BFS_KEEP_CHILD=0"), "bfs"),
 ], ids=["fstack1", "tile_search", "tile_search_inreg", "guided_batch_lanemajor", "cs_binary_split", "bfs_pop1",
-        "bfs_pop32", "bfs_pop_newest", "bfs_keep_child"])
+        "bfs_pop32", "bfs_pop_oldest", "bfs_pop_oldest_nokeep"])
 def test_variant_parity(cuda_device, defines, what):
     lib = _variant(defines)
     res = _probe(lib, what)

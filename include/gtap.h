@@ -148,6 +148,11 @@ gtap_status gtap_reset(gtap_runtime *rt, void *stream);
 
 /* Launch the persistent kernel for the staged roots on `stream` (async).
  * Implies gtap_reset unless the runtime was reset since the last run.
+ * Everything a run enqueues is SM work on `stream`: a small kernel stages the
+ * roots and control block from the runtime's mapped pinned host buffers, the
+ * table's scratch/board and workspace resets are fill kernels, and the control
+ * block returns the same way after the scheduler -- no copy-engine transfer,
+ * so a run never queues behind the caller's bulk copies on other streams.
  * Returns GTAP_E_BUSY if a run is in flight, GTAP_E_INVAL if no root is
  * staged or the grid cannot be co-resident. */
 gtap_status gtap_run(gtap_runtime *rt, void *stream);

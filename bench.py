@@ -352,7 +352,9 @@ def bench_fib20(dev, reps=20):
     """BASELINE configs[0] / SURVEY §8(d) C1: fib(20) (21,891 tasks) is span-bound -- its critical path is
     2n - 1 = 39 dependent invocations -- so it is reported as tasks/s and as time per critical-path step."""
     import paper_2604_05982_b200 as g
-    rt = g.Runtime(g.GTAP_WORKER_THREAD, dev.index, **FIB_CFG)
+    # a short idle backoff: at fib(20) idle warps polling for the few runnable tasks are on the critical
+    # path (8192 ns cap: 0.198 ms, 1024 ns: 0.145 ms; fib(40) prefers 8192, bench_tools/fib_backoff.py)
+    rt = g.Runtime(g.GTAP_WORKER_THREAD, dev.index, **dict(FIB_CFG, idle_backoff_ns=1024))
     ms = []
     st = None
     for i in range(reps + 1):
@@ -366,7 +368,7 @@ def bench_fib20(dev, reps=20):
                 value=st.tasks / (t * 1e-3), ms=t, tasks=st.tasks, invocations=st.invocations,
                 us_per_critical_path_invocation=t * 1e3 / 39.0,
                 note="critical path 2n-1 = 39 dependent invocations (SURVEY §8(a) A12a); includes the persistent "
-                     "kernel's start and drain")
+                     "kernel's start and drain", launch=dict(FIB_CFG, idle_backoff_ns=1024))
 
 
 def bench_epaq(dev, cutoff=10, reps=3):

@@ -187,6 +187,12 @@ __device__ __forceinline__ uint4 ld_relaxed_v4(const void* p) {
                  : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
     return v;
 }
+// one 32-B record (one L2 sector) in a single 256-bit strong load (LDG.E.ENL2.256.STRONG.GPU on sm_100a)
+__device__ __forceinline__ void ld_relaxed_v8(const void* p, uint4& lo, uint4& hi) {
+    asm volatile("ld.relaxed.gpu.global.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(lo.x), "=r"(lo.y), "=r"(lo.z), "=r"(lo.w), "=r"(hi.x), "=r"(hi.y), "=r"(hi.z), "=r"(hi.w)
+                 : "l"(p) : "memory");
+}
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
     uint32_t v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");

@@ -115,6 +115,9 @@ struct assist_of { static constexpr bool value = false; };
 template <class T>
 struct assist_of<T, decltype((void)T::kAssist, void())> { static constexpr bool value = T::kAssist; };
 
+#ifndef GTAP_REC_V8
+#define GTAP_REC_V8 1   // dispatch loads a record with one 256-bit load (0: two 128-bit loads)
+#endif
 #ifndef GTAP_FSTACK
 #define GTAP_FSTACK 256
 #endif
@@ -413,8 +416,13 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
         uint32_t parent = kNone, ord = 0, myfn = 0;
         uint32_t mydata[kDataWords] = {0, 0, 0, 0};
         if (my != kNone) {
+#if GTAP_REC_V8
+            uint4 h, dv;
+            ld_relaxed_v8(p.rec + my, h, dv);   // header + payload: one 256-bit request
+#else
             const uint4 h = ld_relaxed_v4(p.rec + my);
             const uint4 dv = ld_relaxed_v4(&p.rec[my].d[0]);
+#endif
             const uint32_t d[kDataWords] = {dv.x, dv.y, dv.z, dv.w};
             if (T::kHasHeavy) { mydata[0] = dv.x; mydata[1] = dv.y; mydata[2] = dv.z; mydata[3] = dv.w; }
             parent = h.w;

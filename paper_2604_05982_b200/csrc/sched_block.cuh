@@ -329,8 +329,10 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) block_sched_ker
                         bid = ld_relaxed(&ring[(L.tail - 1u - lane) & qmask]);
                     }
                     sm.bq_id[lane] = bid;
-                    sm.bq_h[lane] = ld_relaxed_v4(p.rec + bid);
-                    sm.bq_d[lane] = ld_relaxed_v4(&p.rec[bid].d[0]);
+                    uint4 bh, bd4;
+                    ld_relaxed_v8(p.rec + bid, bh, bd4);   // one 256-bit request per record
+                    sm.bq_h[lane] = bh;
+                    sm.bq_d[lane] = bd4;
                 }
                 __syncwarp();
                 L.tail -= c;
@@ -427,8 +429,8 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) block_sched_ker
                         sm.parent = h.w;
                         sm.d[0] = dv.x; sm.d[1] = dv.y; sm.d[2] = dv.z; sm.d[3] = dv.w;
                     } else {
-                        const uint4 h = ld_relaxed_v4(p.rec + id);
-                        const uint4 dv = ld_relaxed_v4(&p.rec[id].d[0]);
+                        uint4 h, dv;
+                        ld_relaxed_v8(p.rec + id, h, dv);   // one 256-bit request per record
                         sm.fn = meta_fn(h.z); sm.state = meta_state(h.z); sm.ord = meta_ord(h.z);
                         sm.parent = h.w;
                         sm.d[0] = dv.x; sm.d[1] = dv.y; sm.d[2] = dv.z; sm.d[3] = dv.w;

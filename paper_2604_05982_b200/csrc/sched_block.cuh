@@ -213,8 +213,8 @@ __device__ bool block_publish_spawns(const KParams& p, BLeader& L, BlockSmem<T>&
         if (lane < c) {
             const ChildSpec cs = sm.spawns[b + lane];
             TaskRec* r = p.rec + id;
-            st_v4(r, make_uint4(0u, 0u, make_meta(cs.fn, 0, b + lane, 0), parent_id));
-            st_v4(&r->d[0], make_uint4(cs.d[0], cs.d[1], cs.d[2], cs.d[3]));
+            st_v8(r, make_uint4(0u, 0u, make_meta(cs.fn, 0, b + lane, 0), parent_id),
+                  make_uint4(cs.d[0], cs.d[1], cs.d[2], cs.d[3]));   // one 256-bit store per child record
             const uint32_t i = b + lane;
             if (keep_last && i == cnt - 1u) {  // lane-local; broadcast below
                 L.kept = id;

@@ -542,8 +542,13 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
                     cfn = o.cfn[c]; cq = o.cq[c];
                     cd[0] = o.cd[c][0]; cd[1] = o.cd[c][1]; cd[2] = o.cd[c][2]; cd[3] = o.cd[c][3];
                 }
+#if GTAP_REC_V8
+                st_v8(cr, make_uint4(0u, 0u, make_meta(cfn, 0, c, cq), T::kTaskwait ? my : kNone),
+                      make_uint4(cd[0], cd[1], cd[2], cd[3]));   // the child record: one 256-bit store
+#else
                 st_v4(cr, make_uint4(0u, 0u, make_meta(cfn, 0, c, cq), T::kTaskwait ? my : kNone));
                 st_v4(&cr->d[0], make_uint4(cd[0], cd[1], cd[2], cd[3]));
+#endif
                 if constexpr (kGeneric) {
                     sm.cbuf[g] = cid[c] | (task_is_heavy<T>(cfn, cd) ? kHeavyBit : 0u);
                     sm.cqb[g] = (uint8_t)cq;

@@ -70,7 +70,9 @@ typedef struct {
     uint32_t max_tasks_per_worker; /* GTAP_MAX_TASKS_PER_WARP / _PER_BLOCK;
                                       records per worker pool, power of two; 0 = 4096 */
     uint32_t queue_capacity;       /* ring slots per deque, power of two; 0 = max_tasks_per_worker */
-    uint32_t max_child_tasks;      /* GTAP_MAX_CHILD_TASKS; 0 = table's own bound */
+    uint32_t max_child_tasks;      /* GTAP_MAX_CHILD_TASKS: an invocation spawning more fails
+                                      the run with GTAP_E_CHILD_LIMIT; 0 = the table's own bound (a larger
+                                      value is clamped to it) */
     uint32_t num_queues;           /* GTAP_NUM_QUEUES (EPAQ): deques per warp, 1..8;
                                       block-level workers: 1; 0 = 1 */
     uint32_t max_task_data_size;   /* GTAP_MAX_TASK_DATA_SIZE bytes; 0 = 16 */
@@ -143,7 +145,9 @@ gtap_status gtap_spawn_root(gtap_runtime *rt, const gtap_task_table *table, uint
                             const void *args, uint32_t nbytes, uint32_t *root_idx);
 
 /* Re-arm the workspace for a new run (zero queues, pools, counters; drop
- * staged roots). Asynchronous on `stream`. */
+ * staged roots). Asynchronous on `stream`; the next gtap_run waits for it
+ * (an event recorded here, waited for on the run's stream), so reset and run
+ * may use different streams. */
 gtap_status gtap_reset(gtap_runtime *rt, void *stream);
 
 /* Launch the persistent kernel for the staged roots on `stream` (async).
@@ -154,7 +158,9 @@ gtap_status gtap_reset(gtap_runtime *rt, void *stream);
  * block returns the same way after the scheduler -- no copy-engine transfer,
  * so a run never queues behind the caller's bulk copies on other streams.
  * Returns GTAP_E_BUSY if a run is in flight, GTAP_E_INVAL if no root is
- * staged or the grid cannot be co-resident. */
+ * staged or the grid cannot be co-resident. Any other failure drops the
+ * staged roots and the table binding (stage them again after fixing the
+ * cause); the workspace is fully reset before the next run. */
 gtap_status gtap_run(gtap_runtime *rt, void *stream);
 
 /* Block until the run finishes; decode the device error word; fill *out

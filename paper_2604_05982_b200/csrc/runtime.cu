@@ -38,6 +38,8 @@ struct gtap_runtime {
     RootSpec* dh_roots;    // device aliases of the two mapped buffers
     Ctl* dh_ctl;
     cudaEvent_t ev0, ev1, ev2;   // kernel start / end, control-block readback done
+    cudaEvent_t ev_reset;        // recorded after gtap_reset's fill kernels: gtap_run's stream waits on it
+    bool reset_pending;          // ev_reset recorded and not yet waited for by a run
     bool in_flight;
     bool dirty;            // workspace used since the last reset
     uint32_t run_grid, run_block, run_W;
@@ -156,6 +158,9 @@ gtap_status do_reset(gtap_runtime* rt, cudaStream_t s) {
     // free rings: entry 0 = empty
     if (gtap::zero_async(rt->ws + L.fring, sizeof(uint32_t) * (size_t)L.W * L.M, s) != cudaSuccess)
         return GTAP_E_CUDA;
+    // a run on another stream must not start before these fills (gtap_run waits on the event)
+    if (cudaEventRecord(rt->ev_reset, s) != cudaSuccess) return GTAP_E_CUDA;
+    rt->reset_pending = true;
     rt->dirty = false;
     return GTAP_OK;
 }
@@ -248,7 +253,8 @@ gtap_status gtap_init(const gtap_config* in, void* d_workspace, size_t bytes, gt
         return GTAP_E_NOMEM;
     }
     if (cudaEventCreate(&rt->ev0) != cudaSuccess || cudaEventCreate(&rt->ev1) != cudaSuccess ||
-        cudaEventCreate(&rt->ev2) != cudaSuccess) {
+        cudaEventCreate(&rt->ev2) != cudaSuccess ||
+        cudaEventCreateWithFlags(&rt->ev_reset, cudaEventDisableTiming) != cudaSuccess) {
         gtap_finalize(rt);
         return GTAP_E_CUDA;
     }
@@ -299,16 +305,16 @@ gtap_status gtap_geometry(gtap_runtime* rt, const gtap_task_table* t, uint32_t* 
     return GTAP_OK;
 }
 
-gtap_status gtap_run(gtap_runtime* rt, void* stream) {
-    if (!rt) return GTAP_E_INVAL;
-    if (rt->in_flight) return GTAP_E_BUSY;
-    if (rt->roots.empty() || !rt->table) return GTAP_E_INVAL;
-    cudaSetDevice(rt->device);
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
+static gtap_status run_impl(gtap_runtime* rt, cudaStream_t s) {
     uint32_t W = 0, grid = 0, block = 0;
     gtap_status st = geometry(rt, rt->table, &W, &grid, &block);
     if (st != GTAP_OK) return st;
     if (rt->dirty && (st = do_reset(rt, s)) != GTAP_OK) return st;
+    // gtap_reset may have been enqueued on another stream: order its fills before this run
+    if (rt->reset_pending) {
+        if (cudaStreamWaitEvent(s, rt->ev_reset, 0) != cudaSuccess) return GTAP_E_CUDA;
+        rt->reset_pending = false;
+    }
     const uint32_t nroots = (uint32_t)rt->roots.size();
     // roots + termination counters: one pinned H2D copy each
     std::memcpy(rt->h_roots, rt->roots.data(), sizeof(RootSpec) * nroots);
@@ -330,7 +336,12 @@ gtap_status gtap_run(gtap_runtime* rt, void* stream) {
     p.steal_rounds = rt->cfg.steal_attempts;
     p.steal_max = rt->cfg.steal_max;
     p.nroots = nroots;
-    p.max_child = rt->cfg.max_child_tasks ? rt->cfg.max_child_tasks : rt->table->max_children;
+    // GTAP_MAX_CHILD_TASKS: the config's limit, never above the table's compile-time bound (0 = dynamic table:
+    // only the config's limit, if any, applies)
+    {
+        const uint32_t tb = rt->table->max_children, cl = rt->cfg.max_child_tasks;
+        p.max_child = tb == 0u ? cl : (cl ? std::min(cl, tb) : tb);
+    }
     p.seed = rt->cfg.seed;
     p.watchdog_ns = rt->cfg.watchdog_ns;
     p.idle_backoff = rt->cfg.idle_backoff_ns;
@@ -363,6 +374,30 @@ gtap_status gtap_run(gtap_runtime* rt, void* stream) {
     rt->run_nroots = nroots;
     rt->roots.clear();
     return GTAP_OK;
+}
+
+}  // extern "C"
+
+namespace {
+// any failure of gtap_run drops the staged roots and the table binding (the caller may destroy the
+// table next; a later run must not pick up stale roots) and forces a full reset before the next run
+gtap_status run_failed(gtap_runtime* rt, gtap_status st) {
+    rt->roots.clear();
+    rt->table = nullptr;
+    rt->dirty = true;
+    return st;
+}
+}  // namespace
+
+extern "C" {
+
+gtap_status gtap_run(gtap_runtime* rt, void* stream) {
+    if (!rt) return GTAP_E_INVAL;
+    if (rt->in_flight) return GTAP_E_BUSY;
+    if (rt->roots.empty() || !rt->table) return run_failed(rt, GTAP_E_INVAL);
+    cudaSetDevice(rt->device);
+    const gtap_status st = run_impl(rt, static_cast<cudaStream_t>(stream));
+    return st == GTAP_OK ? st : run_failed(rt, st);
 }
 
 gtap_status gtap_sync(gtap_runtime* rt, gtap_stats* out) {
@@ -423,6 +458,7 @@ gtap_status gtap_finalize(gtap_runtime* rt) {
     if (rt->ev0) cudaEventDestroy(rt->ev0);
     if (rt->ev1) cudaEventDestroy(rt->ev1);
     if (rt->ev2) cudaEventDestroy(rt->ev2);
+    if (rt->ev_reset) cudaEventDestroy(rt->ev_reset);
     delete rt;
     return GTAP_OK;
 }

@@ -482,7 +482,10 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) block_sched_ker
 
         // ================= warp 0: spawn / join / finish =================
         if (warp == 0) {
-            const uint32_t err = sm.err ? sm.err : (sm.action == 0 ? (uint32_t)GTAP_E_BAD_STATE : 0u);
+            uint32_t err = sm.err ? sm.err : (sm.action == 0 ? (uint32_t)GTAP_E_BAD_STATE : 0u);
+            // GTAP_MAX_CHILD_TASKS: the run's limit on spawns per invocation (tables without taskwait
+            // publish mid-body through flush(); their limit is checked per staging round)
+            if (err == 0u && p.max_child && sm.nspawn > p.max_child) err = GTAP_E_CHILD_LIMIT;
             const uint32_t staged = min(sm.nspawn, (uint32_t)T::kSpawnCap);
             bool ok = (err == 0u);
             if (!ok && lane == 0) raise_error(p.ctl, err);

@@ -115,9 +115,6 @@ struct assist_of { static constexpr bool value = false; };
 template <class T>
 struct assist_of<T, decltype((void)T::kAssist, void())> { static constexpr bool value = T::kAssist; };
 
-#ifndef GTAP_REC_V8
-#define GTAP_REC_V8 1   // dispatch loads a record with one 256-bit load (0: two 128-bit loads)
-#endif
 #ifndef GTAP_FSTACK
 #define GTAP_FSTACK 256
 #endif
@@ -416,13 +413,8 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
         uint32_t parent = kNone, ord = 0, myfn = 0;
         uint32_t mydata[kDataWords] = {0, 0, 0, 0};
         if (my != kNone) {
-#if GTAP_REC_V8
             uint4 h, dv;
             ld_relaxed_v8(p.rec + my, h, dv);   // header + payload: one 256-bit request
-#else
-            const uint4 h = ld_relaxed_v4(p.rec + my);
-            const uint4 dv = ld_relaxed_v4(&p.rec[my].d[0]);
-#endif
             const uint32_t d[kDataWords] = {dv.x, dv.y, dv.z, dv.w};
             if (T::kHasHeavy) { mydata[0] = dv.x; mydata[1] = dv.y; mydata[2] = dv.z; mydata[3] = dv.w; }
             parent = h.w;
@@ -437,6 +429,8 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
                     if ((uint32_t)c < o.nchild && o.cq[c] >= (uint32_t)NQ) o.err = GTAP_E_INVAL;
             }
             if (kGen && o.nchild > (uint32_t)MAXC) o.err = GTAP_E_CHILD_LIMIT;
+            // GTAP_MAX_CHILD_TASKS: the run's limit (config.max_child_tasks, <= the table's bound)
+            if (p.max_child && o.nchild > p.max_child) o.err = GTAP_E_CHILD_LIMIT;
         }
         if constexpr (assist_of<T>::value) {
             // (2b) warp assist: lanes whose body deferred a heavy leaf routine get the whole warp,
@@ -542,13 +536,8 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
                     cfn = o.cfn[c]; cq = o.cq[c];
                     cd[0] = o.cd[c][0]; cd[1] = o.cd[c][1]; cd[2] = o.cd[c][2]; cd[3] = o.cd[c][3];
                 }
-#if GTAP_REC_V8
                 st_v8(cr, make_uint4(0u, 0u, make_meta(cfn, 0, c, cq), T::kTaskwait ? my : kNone),
                       make_uint4(cd[0], cd[1], cd[2], cd[3]));   // the child record: one 256-bit store
-#else
-                st_v4(cr, make_uint4(0u, 0u, make_meta(cfn, 0, c, cq), T::kTaskwait ? my : kNone));
-                st_v4(&cr->d[0], make_uint4(cd[0], cd[1], cd[2], cd[3]));
-#endif
                 if constexpr (kGeneric) {
                     sm.cbuf[g] = cid[c] | (task_is_heavy<T>(cfn, cd) ? kHeavyBit : 0u);
                     sm.cqb[g] = (uint8_t)cq;

@@ -108,7 +108,8 @@ struct CsArgs {
     int32_t* keys;
     int32_t* scratch;
     uint32_t cut_sort, cut_merge;
-    uint32_t mode, pad;
+    uint32_t mode;
+    uint32_t n;         // array length (roots are validated against it)
 };
 
 // MODE: GTAP_MERGE_THREAD (0: leaf sorts and sequential merges on the task's lane) or
@@ -225,8 +226,11 @@ struct CilksortTable {
     }
 };
 
-static int validate_cs(const gtap_task_table*, uint32_t fn, const uint32_t* d) {
-    return (fn == 0u && d[0] <= d[1] && d[2] == 0u) ? 0 : -1;
+// a root {l, r} must lie inside keys[0, n) (n < 2^25: the packed merge descriptor's index width)
+static int validate_cs(const gtap_task_table* t, uint32_t fn, const uint32_t* d) {
+    CsArgs a;
+    std::memcpy(&a, t->args, sizeof(a));
+    return (fn == 0u && d[0] <= d[1] && d[1] <= a.n && d[2] == 0u) ? 0 : -1;
 }
 
 }  // namespace gtap
@@ -238,7 +242,7 @@ extern "C" const gtap_task_table* gtap_table_cilksort_ex(int32_t* keys, int32_t*
     if (((!keys || !scratch) && n > 0) || n >= (1ull << 25) || cut_sort < 1 ||
         cut_sort > (int32_t)gtap::kCsMaxSortCut || cut_merge < 2 || merge_mode > 1u)
         return nullptr;
-    gtap::CsArgs a{keys, scratch, (uint32_t)cut_sort, (uint32_t)cut_merge, merge_mode, 0u};
+    gtap::CsArgs a{keys, scratch, (uint32_t)cut_sort, (uint32_t)cut_merge, merge_mode, (uint32_t)n};
     return merge_mode == 1u ? gtap::make_table<gtap::CilksortTable<1u>>("cilksort_warp", a, &gtap::validate_cs)
                             : gtap::make_table<gtap::CilksortTable<0u>>("cilksort", a, &gtap::validate_cs);
 }

@@ -1369,9 +1369,11 @@ struct MergesortTable {
     }
 };
 
+// a root {l, r} must lie inside keys[0, n): the kernel reads and writes [l, r) of keys and scratch
 static int validate_ms(const gtap_task_table* t, uint32_t fn, const uint32_t* d) {
-    (void)t;
-    return (fn == 0u && d[0] <= d[1] && d[2] == 0u) ? 0 : -1;
+    MsArgs a;
+    std::memcpy(&a, t->args, sizeof(a));
+    return (fn == 0u && d[0] <= d[1] && d[1] <= a.n && d[2] == 0u) ? 0 : -1;
 }
 
 }  // namespace gtap

@@ -209,6 +209,8 @@ class Table:
     @staticmethod
     def cilksort(keys, scratch, cut_sort: int = 64, cut_merge: int = 256, merge_mode: int = 1) -> "Table":
         _dev_i32(keys, "keys"); _dev_i32(scratch, "scratch")
+        if scratch.numel() < keys.numel():
+            raise ValueError("scratch must hold n keys")
         return Table(lib().gtap_table_cilksort_ex(keys.data_ptr(), scratch.data_ptr(), keys.numel(), cut_sort, cut_merge,
                                                   merge_mode),
                      "cilksort", GTAP_WORKER_THREAD, (keys, scratch))
@@ -263,7 +265,7 @@ class Runtime:
     def __init__(self, kind: int, device: int = 0, *, grid_size: int = 0, block_size: int = 0,
                  max_tasks_per_worker: int = 0, queue_capacity: int = 0, steal_attempts: int = 0,
                  steal_max: int = 0, seed: int = 0x5EED, watchdog_ns: int = 0, max_roots: int = 0,
-                 idle_backoff_ns: int = 0, num_queues: int = 0,
+                 idle_backoff_ns: int = 0, num_queues: int = 0, max_child_tasks: int = 0,
                  torch_workspace: bool = True):
         import torch
         L = lib()
@@ -272,7 +274,7 @@ class Runtime:
         for k, v in dict(grid_size=grid_size, block_size=block_size, max_tasks_per_worker=max_tasks_per_worker,
                          queue_capacity=queue_capacity, steal_attempts=steal_attempts, steal_max=steal_max,
                          watchdog_ns=watchdog_ns, max_roots=max_roots, idle_backoff_ns=idle_backoff_ns,
-                         num_queues=num_queues).items():
+                         num_queues=num_queues, max_child_tasks=max_child_tasks).items():
             if v:
                 setattr(cfg, k, v)
         cfg.seed = seed

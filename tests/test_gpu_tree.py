@@ -125,3 +125,17 @@ def test_block_batch_steal(g, buf, buf_cpu, steal_max):
         assert (total, st.tasks) == oracle.tree(14, _np(buf_cpu), 5, 70)
         total, st = g.tree(16, buf, 5, 70, pruned=True, seed=9, worker=g.GTAP_WORKER_BLOCK, rt=r)
         assert (total, st.tasks) == oracle.tree(16, _np(buf_cpu), 5, 70, pruned=True, seed=9)
+
+
+@pytest.mark.parametrize("kind", KINDS)
+def test_bench_per_node_work(g, kind):
+    """The bench's per-node work (mem_ops 64 with compute_iters 256 on the full tree, 32768 on the pruned
+    tree: bench.bench_tree) at reduced depth so the oracle finishes in seconds; bench launch configuration."""
+    import bench
+    b_cpu = synth.tree_buffer(1 << 20)
+    b = b_cpu.to("cuda")
+    with g.Runtime(_kind(g, kind), 0, watchdog_ns=WD, **bench.TREE_CFG[kind]) as r:
+        total, st = g.tree(12, b, 64, 256, worker=_kind(g, kind), rt=r)
+        assert (total, st.tasks) == oracle.tree(12, _np(b_cpu), 64, 256)
+        total, st = g.tree(9, b, 64, 32768, pruned=True, seed=1, worker=_kind(g, kind), rt=r)
+        assert (total, st.tasks) == oracle.tree(9, _np(b_cpu), 64, 32768, pruned=True, seed=1)

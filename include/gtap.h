@@ -285,7 +285,8 @@ gtap_status gtap_bfs_init_depth(int32_t *depth, uint32_t nv, int32_t src, void *
 
 /* L2-atomic throughput probe on `stream`, synchronous. kind: 0 atom.add with
  * return on distinct words (the join decrement), 1 red.add (no return),
- * 2 atom.cas, 3 atom.min, 4 same-address atom.add. d_buf: device buffer of
+ * 2 atom.cas, 3 atom.min, 4 same-address atom.add, 5 atom.acq_rel.add, 6 relaxed
+ * 64-bit atom.add with return (the fused fib join word). d_buf: device buffer of
  * >= words*4 bytes (zeroed by the call). ops_per_thread atomics per thread on
  * grid x block threads. *ms = kernel time. */
 gtap_status gtap_ubench_atomics(void *d_buf, uint64_t words, uint32_t kind, uint32_t grid,

@@ -4,6 +4,7 @@ User-facing calls (each runs the whole path in libgtap.so's CUDA kernels and
 fails loudly when the library or the GPU is missing -- there is no CPU path):
 
     fib(n)                       -> (F(n), stats)      thread-level, P:1023-1033
+    fib_forest([n, ...])         -> ([F(n)], stats)    independent roots (forest)
     mergesort_(keys)             -> stats (in place)   thread-level, P:153-165
     mergesort_forest_(keys, seg) -> stats              independent roots (forest)
     spmv(row_ptr, col, val, x)   -> (y, stats)         block-level, P:42
@@ -19,7 +20,7 @@ from . import gtap
 from .gtap import (GTAP_WORKER_BLOCK, GTAP_WORKER_THREAD, GtapError, Runtime, RunStats, Table,
                    bfs_init_depth, ubench_atomics)
 
-__all__ = ["gtap", "Runtime", "Table", "RunStats", "GtapError", "fib", "fib_cutoff", "nqueens", "tree", "mergesort_", "cilksort_", "mergesort_forest_",
+__all__ = ["gtap", "Runtime", "Table", "RunStats", "GtapError", "fib", "fib_forest", "fib_cutoff", "nqueens", "tree", "mergesort_", "cilksort_", "mergesort_forest_",
            "spmv", "bfs", "ubench_atomics", "GTAP_WORKER_THREAD", "GTAP_WORKER_BLOCK"]
 
 
@@ -38,6 +39,24 @@ def fib(n: int, rt: Runtime | None = None, device: int = 0, stream=None, **cfg):
         rt.run(stream)
         st = rt.sync()
         return rt.root_result(0), st
+    finally:
+        table.close()
+        if own:
+            rt.close()
+
+
+def fib_forest(ns, rt: Runtime | None = None, device: int = 0, stream=None, **cfg):
+    """A forest of independent fib roots in ONE run (root r starts on worker r mod W):
+    returns ([F(n) for n in ns], stats)."""
+    cfg.setdefault("max_roots", max(len(ns), 1))
+    rt, own = _runtime(GTAP_WORKER_THREAD, rt, device, cfg)
+    table = Table.fib()
+    try:
+        for n in ns:
+            rt.spawn_root(table, (n,))
+        rt.run(stream)
+        st = rt.sync()
+        return [rt.root_result(i) for i in range(len(ns))], st
     finally:
         table.close()
         if own:

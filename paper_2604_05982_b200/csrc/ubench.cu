@@ -35,6 +35,9 @@ __global__ void __launch_bounds__(1024) ubench_kernel(uint32_t* buf, uint64_t wo
             acc += gtap::dev::atom_add_relaxed(buf, 1u);
         } else if constexpr (KIND == 5) {
             acc += (uint32_t)gtap::dev::atom_add_acq_rel(reinterpret_cast<int32_t*>(p), 1);
+        } else if constexpr (KIND == 6) {
+            // the fused fib join: one relaxed 64-bit atom.add with return per task
+            acc += (uint32_t)gtap::dev::atom_add_relaxed_u64(p, 0x1FFFFFFFFull);
         }
     }
     if (acc == 0xFFFFFFFFu) atomicAdd(sink, 1ull);
@@ -44,7 +47,7 @@ __global__ void __launch_bounds__(1024) ubench_kernel(uint32_t* buf, uint64_t wo
 
 extern "C" gtap_status gtap_ubench_atomics(void* d_buf, uint64_t words, uint32_t kind, uint32_t grid, uint32_t block,
                                            uint32_t ops_per_thread, void* stream, float* ms) {
-    if (!d_buf || words < 8 || kind > 5 || grid == 0 || block == 0 || block > 1024 || !ms) return GTAP_E_INVAL;
+    if (!d_buf || words < 8 || kind > 6 || grid == 0 || block == 0 || block > 1024 || !ms) return GTAP_E_INVAL;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     uint32_t* buf = static_cast<uint32_t*>(d_buf);
     if (cudaMemsetAsync(buf, 0, words * 4, s) != cudaSuccess) return GTAP_E_CUDA;
@@ -60,6 +63,7 @@ extern "C" gtap_status gtap_ubench_atomics(void* d_buf, uint64_t words, uint32_t
         case 3: ubench_kernel<3><<<grid, block, 0, s>>>(buf, words - 8, ops_per_thread, sink); break;
         case 4: ubench_kernel<4><<<grid, block, 0, s>>>(buf, words - 8, ops_per_thread, sink); break;
         case 5: ubench_kernel<5><<<grid, block, 0, s>>>(buf, words - 8, ops_per_thread, sink); break;
+        case 6: ubench_kernel<6><<<grid, block, 0, s>>>(buf, words - 8, ops_per_thread, sink); break;
     }
     cudaEventRecord(e1, s);
     const cudaError_t err = cudaEventSynchronize(e1);

@@ -66,3 +66,37 @@ def max_over_ranks(x: float, device="cpu", group=None) -> float:
     t = torch.tensor([float(x)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return float(t.item())
+
+
+def gather_round_robin(rows, n_items: int, world: int, rank: int, device="cpu", group=None):
+    """all_gather of per-item result rows of round-robin-dealt items -> list indexed by item.
+
+    `rows[j]` is this rank's row (a list of floats, all rows of one width) for item
+    split_round_robin(n_items, world, rank)[j]. Each rank pads its rows to the largest share, ONE
+    all_gather moves them, and the rows are put back in item order on every rank.
+    """
+    import torch
+    import torch.distributed as dist
+    mine = split_round_robin(n_items, world, rank)
+    if len(rows) != len(mine):
+        raise ValueError("one row per owned item")
+    width = len(rows[0]) if rows else 0
+    widths = torch.tensor([width], dtype=torch.int64, device=device)
+    if world > 1:
+        dist.all_reduce(widths, op=dist.ReduceOp.MAX, group=group)
+    width = int(widths.item())
+    share = len(split_round_robin(n_items, world, 0))
+    flat = torch.zeros(share * width, dtype=torch.float64, device=device)
+    if rows:
+        flat[: len(rows) * width] = torch.tensor([float(v) for r in rows for v in r], dtype=torch.float64)
+    if world > 1:
+        bufs = [torch.empty_like(flat) for _ in range(world)]
+        dist.all_gather(bufs, flat, group=group)
+    else:
+        bufs = [flat]
+    out = [None] * n_items
+    for r in range(world):
+        b = bufs[r].view(share, width).tolist() if width else [[] for _ in range(share)]
+        for j, k in enumerate(split_round_robin(n_items, world, r)):
+            out[k] = b[j]
+    return out

@@ -114,3 +114,88 @@ def test_split_round_robin():
     assert shard.split_round_robin(7, 2, 1) == [1, 3, 5]
     with pytest.raises(ValueError):
         shard.split_round_robin(3, 2, 2)
+
+
+def bfs_source_split(rank, world):
+    """C5a at N ranks: the graph replicated, 16 sources dealt round robin, one gather of per-source rows."""
+    import oracle
+    import synth
+    rp, col = synth.rmat_csr(10, 16, seed=3)
+    srcs = synth.bfs_sources(rp, 16, seed=5)
+    mine = shard.split_round_robin(16, world, rank)
+    rows = []
+    for k in mine:
+        lv = oracle.bfs(rp, col, srcs[k])
+        reached = lv != 0x7FFFFFFF
+        rows.append([float(k), float(reached.sum()), float(lv[reached].astype(np.int64).sum())])
+    return shard.gather_round_robin(rows, 16, world, rank)
+
+
+def fib_forest_split(rank, world):
+    """A fib forest at N ranks: roots dealt round robin, one gather of the 4-B root results."""
+    import oracle
+    ns = [5 + (k % 11) for k in range(13)]
+    mine = shard.split_round_robin(len(ns), world, rank)
+    return shard.gather_round_robin([[float(oracle.fib(ns[k])[0])] for k in mine], len(ns), world, rank)
+
+
+@pytest.mark.timeout(300)
+def test_bfs_sources_split_world2():
+    import oracle
+    import synth
+    out = run_world(bfs_source_split)
+    rp, col = synth.rmat_csr(10, 16, seed=3)
+    srcs = synth.bfs_sources(rp, 16, seed=5)
+    for r in (0, 1):
+        rows = out[r]
+        assert isinstance(rows, list) and len(rows) == 16, rows
+        for k, row in enumerate(rows):
+            lv = oracle.bfs(rp, col, srcs[k])
+            reached = lv != 0x7FFFFFFF
+            assert row == [float(k), float(reached.sum()), float(lv[reached].astype(np.int64).sum())]
+
+
+@pytest.mark.timeout(300)
+def test_fib_forest_split_world3():
+    out = run_world(fib_forest_split, world=3)
+    ns = [5 + (k % 11) for k in range(13)]
+    fibs = [0, 1]
+    while len(fibs) < 20:
+        fibs.append(fibs[-1] + fibs[-2])
+    for r in range(3):
+        assert out[r] == [[float(fibs[n])] for n in ns], out[r]
+
+
+def test_gather_round_robin_single_rank():
+    rows = [[float(k), 2.0 * k] for k in range(5)]
+    assert shard.gather_round_robin(rows, 5, 1, 0) == rows
+    with pytest.raises(ValueError):
+        shard.gather_round_robin(rows[:3], 5, 1, 0)
+
+
+def test_bench_world_size_mismatch_fails():
+    """bench.py refuses a world size other than --gpus (the driver's N must be the ranks that ran)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    p = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--impl", "reference"],
+                       env=env, capture_output=True, text=True, timeout=120)
+    assert p.returncode != 0 and "world size 1 != --gpus 2" in p.stderr
+
+
+@pytest.mark.timeout(600)
+def test_bench_reference_self_launch_two_ranks():
+    """bench.py --gpus 2 outside torchrun re-launches itself as 2 ranks; rank 0 alone prints the line."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    p = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--impl", "reference",
+                        "--steps", "1", "--warmup", "0"], env=env, capture_output=True, text=True, timeout=540)
+    assert p.returncode == 0, p.stderr[-2000:]
+    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, p.stdout
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0

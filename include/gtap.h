@@ -51,7 +51,8 @@ typedef enum {
     GTAP_E_TIMEOUT = 8,        /* liveness watchdog expired (config.watchdog_ns) */
     GTAP_E_BAD_STATE = 9,      /* unknown (task function, state) dispatched (P:1188 default:) */
     GTAP_E_NO_DEVICE = 10,     /* no CUDA device / not sm_100 */
-    GTAP_E_UNSUPPORTED = 11    /* table/config combination not built */
+    GTAP_E_UNSUPPORTED = 11,   /* table/config combination not built */
+    GTAP_E_INVARIANT = 12      /* GTAP_CHECK builds: a scheduler invariant failed (gtap_check_read) */
 } gtap_status;
 
 typedef enum {
@@ -170,6 +171,22 @@ gtap_status gtap_sync(gtap_runtime *rt, gtap_stats *out);
 /* Copy root result `root_idx` (int64 on the device) into *out
  * (nbytes <= 8, little-endian truncation). Valid after gtap_sync. */
 gtap_status gtap_root_result(gtap_runtime *rt, uint32_t root_idx, void *out, uint32_t nbytes);
+
+/* Scheduler-invariant counters of the last run (the
+ * correctness sketch of P:137-141): available only in the diagnostic build
+ * compiled with -DGTAP_CHECK (libgtap_gtap_check.so), else GTAP_E_UNSUPPORTED.
+ * That build keeps per-record tokens (allocated, published-and-unclaimed,
+ * children of the current join epoch) and checks them at every scheduler
+ * event; a violation fails the run with GTAP_E_INVARIANT. Valid after
+ * gtap_sync. out[0..15]: events and violations in this order -- allocs,
+ * frees, publications, dispatches, suspends, child joins, continuation
+ * dispatches, double allocs, double frees, double publications, dispatches of
+ * unpublished tasks, continuations dispatched before their last child joined,
+ * join underflows, suspends over a live join; out[16] = records still
+ * allocated, out[17] = tasks still published, out[18] = records with a join
+ * count != 0, out[19] = outstanding counter, out[20] = roots not finished.
+ * n: capacity of out (>= 21). */
+gtap_status gtap_check_read(gtap_runtime *rt, uint64_t *out, uint32_t n);
 
 /* Release everything gtap_init allocated. rt may be NULL. */
 gtap_status gtap_finalize(gtap_runtime *rt);

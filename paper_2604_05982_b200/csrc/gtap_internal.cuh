@@ -98,6 +98,26 @@ struct RootSpec {
     uint32_t d[kDataWords];
 };
 
+// GTAP_CHECK diagnostic build (§4.3.2 P:137-141 correctness sketch):
+// per-record protocol tokens kept beside the workspace, checked at every scheduler event --
+//   live[id]      1 while the record is allocated     (alloc / free must alternate: conservation),
+//   runnable[id]  1 while the task is published and unclaimed (publish / dispatch alternate: every
+//                 published (record, state) is claimed and dispatched exactly once),
+//   kids[id]      children of the record's current join epoch not yet finished (a continuation may
+//                 only be dispatched at 0; an independent count, not the scheduler's join word).
+// Counters of events and violations live in ctr[]; a violation also raises GTAP_E_INVARIANT.
+enum CheckCtr : int {
+    CK_ALLOC = 0, CK_FREE, CK_PUBLISH, CK_DISPATCH, CK_SUSPEND, CK_JOIN, CK_RESUME,
+    CK_V_DOUBLE_ALLOC, CK_V_DOUBLE_FREE, CK_V_DOUBLE_PUBLISH, CK_V_DISPATCH_UNPUBLISHED, CK_V_EARLY_RESUME,
+    CK_V_JOIN_UNDERFLOW, CK_V_SUSPEND_DIRTY, CK_COUNT = 16
+};
+struct CheckBuf {
+    unsigned long long ctr[CK_COUNT];
+    uint32_t* live;
+    uint32_t* runnable;
+    int32_t* kids;
+};
+
 // Kernel parameters (by value): geometry + device pointers into one workspace.
 struct KParams {
     uint32_t W;              // workers (warps or blocks)
@@ -120,6 +140,7 @@ struct KParams {
     Ctl* ctl;
     const RootSpec* roots;   // nroots
     long long* root_results; // nroots
+    CheckBuf* chk;           // GTAP_CHECK builds only (else nullptr)
 };
 
 // Host-side layout of the workspace (offsets in bytes).
@@ -338,6 +359,62 @@ __device__ __forceinline__ void raise_error(Ctl* ctl, uint32_t code) {
     atom_cas_relaxed(&ctl->error, 0u, code);
     st_release(&ctl->done, 1u);
 }
+
+// ---- GTAP_CHECK hooks (compiled only into the diagnostic check build) -------
+#ifdef GTAP_CHECK
+#define GTAP_CK(...) do { __VA_ARGS__; } while (0)
+__device__ __forceinline__ void ck_violation(const KParams& p, int k) {
+    atomicAdd(&p.chk->ctr[k], 1ull);
+    raise_error(p.ctl, GTAP_E_INVARIANT);
+}
+// a record leaves the free pool (root entry, child spawn); the fence orders the token before the
+// record's later hand-over (its ring / free-ring store)
+__device__ __forceinline__ void ck_alloc(const KParams& p, uint32_t id) {
+    __threadfence();
+    atomicAdd(&p.chk->ctr[CK_ALLOC], 1ull);
+    if (atomicExch(&p.chk->live[id], 1u) != 0u) ck_violation(p, CK_V_DOUBLE_ALLOC);
+}
+__device__ __forceinline__ void ck_free(const KParams& p, uint32_t id) {
+    atomicAdd(&p.chk->ctr[CK_FREE], 1ull);
+    if (atomicExch(&p.chk->live[id], 0u) != 1u) ck_violation(p, CK_V_DOUBLE_FREE);
+    __threadfence();
+}
+// a (record, state) becomes runnable: root entry, spawn, last-child resume, empty-join resume
+__device__ __forceinline__ void ck_publish(const KParams& p, uint32_t id) {
+    atomicAdd(&p.chk->ctr[CK_PUBLISH], 1ull);
+    if (atomicExch(&p.chk->runnable[id], 1u) != 0u) ck_violation(p, CK_V_DOUBLE_PUBLISH);
+#if defined(GTAP_CHECK_SELFTEST) && GTAP_CHECK_SELFTEST == 1
+    if (id == 0u && atomicExch(&p.chk->runnable[id], 1u) != 0u) ck_violation(p, CK_V_DOUBLE_PUBLISH);  // injected
+#endif
+    __threadfence();
+}
+// a worker claimed the task and is about to run (record, state)
+__device__ __forceinline__ void ck_dispatch(const KParams& p, uint32_t id, uint32_t state) {
+    __threadfence();
+    atomicAdd(&p.chk->ctr[CK_DISPATCH], 1ull);
+    if (atomicExch(&p.chk->runnable[id], 0u) != 1u) ck_violation(p, CK_V_DISPATCH_UNPUBLISHED);
+    if (state != 0u) {
+        atomicAdd(&p.chk->ctr[CK_RESUME], 1ull);
+        if (ld_relaxed(&p.chk->kids[id]) != 0) ck_violation(p, CK_V_EARLY_RESUME);
+    }
+}
+__device__ __forceinline__ void ck_suspend(const KParams& p, uint32_t id, uint32_t nchildren) {
+    atomicAdd(&p.chk->ctr[CK_SUSPEND], 1ull);
+    if (atomicExch(reinterpret_cast<uint32_t*>(&p.chk->kids[id]), nchildren) != 0u) ck_violation(p, CK_V_SUSPEND_DIRTY);
+    __threadfence();
+}
+// a child of `parent` finished (before the scheduler's own join RMW; the fence orders the two)
+__device__ __forceinline__ void ck_join(const KParams& p, uint32_t parent) {
+#if defined(GTAP_CHECK_SELFTEST) && GTAP_CHECK_SELFTEST == 2
+    if (parent % 5u == 0u) return;   // injected: a lost child join, so that parent's continuation must be flagged
+#endif
+    atomicAdd(&p.chk->ctr[CK_JOIN], 1ull);
+    if (atomicAdd(&p.chk->kids[parent], -1) < 1) ck_violation(p, CK_V_JOIN_UNDERFLOW);
+    __threadfence();
+}
+#else
+#define GTAP_CK(...) do { } while (0)
+#endif
 
 }  // namespace dev
 

@@ -45,6 +45,7 @@ struct gtap_runtime {
     uint32_t run_grid, run_block, run_W;
     uint32_t run_nroots;
     gtap_status last_launch;
+    gtap::CheckBuf* chk;   // GTAP_CHECK builds: device check buffer (header + 3 token arrays)
 };
 
 namespace {
@@ -150,6 +151,12 @@ cudaError_t zero_async(void* p, size_t bytes, cudaStream_t s) {
 
 namespace {
 
+#ifdef GTAP_CHECK
+// header (counters + pointers, padded to 256 B) + live / runnable / kids arrays of W * M words
+size_t check_words(const gtap_runtime* rt) { return (size_t)rt->L.W * rt->L.M; }
+size_t check_bytes(const gtap_runtime* rt) { return 256 + 3 * 4 * check_words(rt); }
+#endif
+
 gtap_status do_reset(gtap_runtime* rt, cudaStream_t s) {
     cudaSetDevice(rt->device);
     const Layout& L = rt->L;
@@ -158,6 +165,9 @@ gtap_status do_reset(gtap_runtime* rt, cudaStream_t s) {
     // free rings: entry 0 = empty
     if (gtap::zero_async(rt->ws + L.fring, sizeof(uint32_t) * (size_t)L.W * L.M, s) != cudaSuccess)
         return GTAP_E_CUDA;
+#ifdef GTAP_CHECK
+    if (rt->chk && gtap::zero_async(rt->chk, check_bytes(rt), s) != cudaSuccess) return GTAP_E_CUDA;
+#endif
     // a run on another stream must not start before these fills (gtap_run waits on the event)
     if (cudaEventRecord(rt->ev_reset, s) != cudaSuccess) return GTAP_E_CUDA;
     rt->reset_pending = true;
@@ -185,6 +195,7 @@ const char* gtap_status_str(gtap_status s) {
         case GTAP_E_BAD_STATE: return "GTAP_E_BAD_STATE";
         case GTAP_E_NO_DEVICE: return "GTAP_E_NO_DEVICE";
         case GTAP_E_UNSUPPORTED: return "GTAP_E_UNSUPPORTED";
+        case GTAP_E_INVARIANT: return "GTAP_E_INVARIANT";
     }
     return "GTAP_E_UNKNOWN";
 }
@@ -258,6 +269,9 @@ gtap_status gtap_init(const gtap_config* in, void* d_workspace, size_t bytes, gt
         gtap_finalize(rt);
         return GTAP_E_CUDA;
     }
+#ifdef GTAP_CHECK
+    if (cudaMalloc(&rt->chk, check_bytes(rt)) != cudaSuccess) { gtap_finalize(rt); return GTAP_E_NOMEM; }
+#endif
     rt->dirty = true;
     if ((st = do_reset(rt, 0)) != GTAP_OK || cudaStreamSynchronize(0) != cudaSuccess) {
         gtap_finalize(rt);
@@ -354,6 +368,21 @@ static gtap_status run_impl(gtap_runtime* rt, cudaStream_t s) {
     p.ctl = reinterpret_cast<Ctl*>(rt->ws + rt->L.ctl);
     p.roots = reinterpret_cast<const RootSpec*>(rt->ws + rt->L.roots);
     p.root_results = reinterpret_cast<long long*>(rt->ws + rt->L.results);
+    p.chk = nullptr;
+#ifdef GTAP_CHECK
+    {   // the header's array pointers (device addresses inside the check buffer), written before the run
+        gtap::CheckBuf hb{};
+        char* base = reinterpret_cast<char*>(rt->chk);
+        hb.live = reinterpret_cast<uint32_t*>(base + 256);
+        hb.runnable = hb.live + check_words(rt);
+        hb.kids = reinterpret_cast<int32_t*>(hb.runnable + check_words(rt));
+        if (cudaMemcpyAsync(reinterpret_cast<char*>(rt->chk) + offsetof(gtap::CheckBuf, live), &hb.live,
+                            3 * sizeof(void*), cudaMemcpyHostToDevice, s) != cudaSuccess ||
+            cudaStreamSynchronize(s) != cudaSuccess)
+            return GTAP_E_CUDA;
+        p.chk = rt->chk;
+    }
+#endif
 
     if (rt->table->prepare && rt->table->prepare(rt->table, s) != cudaSuccess) return GTAP_E_CUDA;
     if (cudaEventRecord(rt->ev0, s) != cudaSuccess) return GTAP_E_CUDA;
@@ -453,6 +482,7 @@ gtap_status gtap_finalize(gtap_runtime* rt) {
     cudaSetDevice(rt->device);
     if (rt->in_flight) cudaEventSynchronize(rt->ev2);
     if (rt->owns_ws && rt->ws) cudaFree(rt->ws);
+    if (rt->chk) cudaFree(rt->chk);
     if (rt->h_roots) cudaFreeHost(rt->h_roots);
     if (rt->h_ctl) cudaFreeHost(rt->h_ctl);
     if (rt->ev0) cudaEventDestroy(rt->ev0);
@@ -461,6 +491,36 @@ gtap_status gtap_finalize(gtap_runtime* rt) {
     if (rt->ev_reset) cudaEventDestroy(rt->ev_reset);
     delete rt;
     return GTAP_OK;
+}
+
+gtap_status gtap_check_read(gtap_runtime* rt, uint64_t* out, uint32_t n) {
+    if (!rt || !out || n < 21) return GTAP_E_INVAL;
+#ifdef GTAP_CHECK
+    if (rt->in_flight) return GTAP_E_BUSY;
+    cudaSetDevice(rt->device);
+    const size_t nw = check_words(rt);
+    std::vector<uint32_t> a(3 * nw);
+    unsigned long long ctr[gtap::CK_COUNT];
+    if (cudaMemcpy(ctr, rt->chk, sizeof(ctr), cudaMemcpyDeviceToHost) != cudaSuccess ||
+        cudaMemcpy(a.data(), reinterpret_cast<char*>(rt->chk) + 256, 4 * a.size(), cudaMemcpyDeviceToHost) != cudaSuccess)
+        return GTAP_E_CUDA;
+    for (int i = 0; i < gtap::CK_COUNT; ++i) out[i] = ctr[i];
+    uint64_t live = 0, runnable = 0, kids = 0;
+    for (size_t i = 0; i < nw; ++i) {
+        live += a[i] != 0u;
+        runnable += a[nw + i] != 0u;
+        kids += a[2 * nw + i] != 0u;
+    }
+    out[16] = live;
+    out[17] = runnable;
+    out[18] = kids;
+    const Ctl& c = *rt->h_ctl;
+    out[19] = (uint64_t)c.outstanding;
+    out[20] = c.roots_left;
+    return GTAP_OK;
+#else
+    return GTAP_E_UNSUPPORTED;
+#endif
 }
 
 void gtap_table_destroy(const gtap_task_table* t) {

@@ -199,8 +199,9 @@ __device__ bool block_publish_spawns(const KParams& p, BLeader& L, BlockSmem<T>&
     }
     uint32_t pushc = keep_last ? cnt - 1u : cnt;
     if (pushc && L.tail + pushc - L.sdone > Q) {
-        if (lane == 0) L.sdone = ld_relaxed(&p.dq[w].steal_done);
+        if (lane == 0) L.sdone = ld_acquire(&p.dq[w].steal_done);
         L.sdone = __shfl_sync(0xffffffffu, L.sdone, 0);
+        __syncwarp();  // lane 0's acquire orders every lane's ring overwrites after the thieves' reads
         if (L.tail + pushc - L.sdone > Q) {
             if (lane == 0) raise_error(p.ctl, GTAP_E_QUEUE_OVERFLOW);
             return false;
@@ -213,6 +214,7 @@ __device__ bool block_publish_spawns(const KParams& p, BLeader& L, BlockSmem<T>&
         if (lane < c) {
             const ChildSpec cs = sm.spawns[b + lane];
             TaskRec* r = p.rec + id;
+            GTAP_CK(ck_alloc(p, id); ck_publish(p, id));
             st_v8(r, make_uint4(0u, 0u, make_meta(cs.fn, 0, b + lane, 0), parent_id),
                   make_uint4(cs.d[0], cs.d[1], cs.d[2], cs.d[3]));   // one 256-bit store per child record
             const uint32_t i = b + lane;
@@ -290,6 +292,7 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) block_sched_ker
             TaskRec* rec = p.rec + id;
             st_v4(rec, make_uint4(0u, 0u, make_meta(rs.fn, 0, 0, 0), kRootFlag | r));
             st_v4(&rec->d[0], make_uint4(rs.d[0], rs.d[1], rs.d[2], rs.d[3]));
+            GTAP_CK(ck_alloc(p, id); ck_publish(p, id));
             ring[i & qmask] = id;
         }
         L.bump = mine;
@@ -436,6 +439,7 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) block_sched_ker
                         sm.d[0] = dv.x; sm.d[1] = dv.y; sm.d[2] = dv.z; sm.d[3] = dv.w;
                     }
                     sm.kept_fresh = 0;
+                    GTAP_CK(ck_dispatch(p, id, sm.state));
                     sm.nspawn = 0; sm.action = 0; sm.has_result = 0; sm.err = 0;
                     ++L.st[ST_CYCLES];
                     ++L.st[ST_INVOC];
@@ -516,8 +520,10 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) block_sched_ker
             if (ok) {
                 if (sm.action == 2) {
                     // suspend: resumption state + join counter
+                    GTAP_CK(if (lane == 0) ck_suspend(p, my, total_children));
                     if (lane == 0) st_v4(p.rec + my, make_uint4(total_children, 0u, make_meta(sm.fn, sm.next_state, sm.ord, 0), sm.parent));
                     if (total_children == 0u) {
+                        GTAP_CK(if (lane == 0) ck_publish(p, my));
                         if (L.kept != kNone) {  // keep the continuation, push the kept child instead
                             if (lane == 0) ring[L.tail & qmask] = L.kept;
                             L.tail += 1u;
@@ -529,11 +535,13 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) block_sched_ker
                     const uint32_t parent = sm.parent;
                     if (parent != kNone && !is_root_link(parent) && sm.has_result && lane == 0)
                         st_relaxed(reinterpret_cast<int32_t*>(&p.rec[parent].d[2 + sm.ord]), sm.result);
+                    GTAP_CK(if (lane == 0) ck_free(p, my));
                     if (lane == 0) block_free1(p, sm, w, my);
                     __syncwarp();
                     uint32_t resume = kNone;
                     if (lane == 0) {
                         if (parent != kNone && !is_root_link(parent)) {
+                            GTAP_CK(ck_join(p, parent));
                             if (atom_add_acq_rel(&p.rec[parent].pending, -1) == 1) resume = parent;
                         } else if (is_root_link(parent)) {
                             p.root_results[parent & ~kRootFlag] = sm.has_result ? (long long)sm.result : 0ll;
@@ -541,6 +549,7 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) block_sched_ker
                                 st_release(&p.ctl->done, 1u);
                         }
                     }
+                    GTAP_CK(if (lane == 0 && resume != kNone) ck_publish(p, resume));
                     resume = __shfl_sync(0xffffffffu, resume, 0);
                     if (resume != kNone) {
                         if (L.kept != kNone) {

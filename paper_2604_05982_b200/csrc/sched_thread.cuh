@@ -250,6 +250,7 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
             TaskRec* rec = p.rec + id;
             st_v4(rec, make_uint4(0u, 0u, make_meta(rs.fn, 0, 0, 0), kRootFlag | r));
             st_v4(&rec->d[0], make_uint4(rs.d[0], rs.d[1], rs.d[2], rs.d[3]));
+            GTAP_CK(ck_alloc(p, id); ck_publish(p, id));
             ring0[i & qmask] = id;
         }
         bump = mine;
@@ -420,6 +421,7 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
             parent = h.w;
             ord = meta_ord(h.z);
             myfn = meta_fn(h.z);
+            GTAP_CK(ck_dispatch(p, my, meta_state(h.z)));
             T::exec(args, meta_fn(h.z), meta_state(h.z), d, o, bx);
             if (o.action == 0u) o.err = GTAP_E_BAD_STATE;
             if (NQ > 1 && !kGen) {  // queue(expr) out of range is a usage error
@@ -472,6 +474,7 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
         const uint32_t fball = __ballot_sync(0xffffffffu, fin);
         const uint32_t F = __popc(fball);
         if (fin) sm.fbuf[__popc(fball & lt)] = my;
+        GTAP_CK(if (fin) ck_free(p, my); __syncwarp());
         const uint32_t nc = (err == 0u) ? o.nchild : 0u;
         // exclusive prefix of the child counts: one ballot per bit of nc (nc <= MAXC)
         uint32_t excl = 0, T_total = 0;
@@ -529,6 +532,7 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
                 const uint32_t g = excl + c;
                 cid[c] = (g < fromF) ? sm.fbuf[g] : sm.abuf[g - fromF];
                 TaskRec* cr = p.rec + cid[c];
+                GTAP_CK(ck_alloc(p, cid[c]); ck_publish(p, cid[c]));
                 uint32_t cfn, cq, cd[kDataWords];
                 if constexpr (kGen) {
                     T::gen_child(o.gen, o.gmask, (uint32_t)c, cfn, cq, cd);
@@ -548,6 +552,7 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
         // queue(expr) rides in the top byte of the join word (EPAQ)
         uint32_t resume_id = kNone, resume_q = 0;
         if (o.action == Out::kSuspend) {
+            GTAP_CK(ck_suspend(p, my, nc));
             st_v4(p.rec + my, make_uint4(nc | (o.next_queue << 24), 0u, make_meta(myfn, o.next_state, ord, 0), parent));
             if (nc == 0u) {  // empty join: runnable at once
                 resume_id = my | (task_is_heavy<T>(myfn, mydata) ? kHeavyBit : 0u);
@@ -565,6 +570,7 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
         const bool jn = fin && err == 0u && parent != kNone && !is_root_link(parent);
         unsigned long long jold = 0;
         if (jn) {
+            GTAP_CK(ck_join(p, parent));
             if constexpr (T::kJoinReduceAdd) {
                 // one relaxed 64-bit RMW: pending -= 1 and acc += result (the count never
                 // underflows, so adding 0xFFFFFFFF carries exactly once into acc: add result - 1)
@@ -627,6 +633,7 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
                 }
             }
         }
+        GTAP_CK(if (resume_id != kNone) ck_publish(p, resume_id & ~kHeavyBit));
         {
             const uint32_t eb = __ballot_sync(0xffffffffu, err != 0u);
             if (eb && lane == (uint32_t)__ffs(eb) - 1u) raise_error(p.ctl, err);
@@ -656,8 +663,9 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
             pushc = R - keep;
             pushq[0] = pushc;
             if (pushc && tail[0] + pushc - sdone[0] > Q) {
-                if (lane == 0) sdone[0] = ld_relaxed(&p.dq[dq0].steal_done);
+                if (lane == 0) sdone[0] = ld_acquire(&p.dq[dq0].steal_done);
                 sdone[0] = __shfl_sync(0xffffffffu, sdone[0], 0);
+                __syncwarp();  // lane 0's acquire orders every lane's ring overwrites after the thieves' reads
                 if (tail[0] + pushc - sdone[0] > Q) {
                     if (lane == 0) raise_error(p.ctl, GTAP_E_QUEUE_OVERFLOW);
                     break;
@@ -710,8 +718,9 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
 #pragma unroll
             for (int q = 0; q < NQ; ++q) {
                 if (pushq[q] && tail[q] + pushq[q] - sdone[q] > Q) {
-                    if (lane == 0) sdone[q] = ld_relaxed(&p.dq[dq0 + q].steal_done);
+                    if (lane == 0) sdone[q] = ld_acquire(&p.dq[dq0 + q].steal_done);
                     sdone[q] = __shfl_sync(0xffffffffu, sdone[q], 0);
+                    __syncwarp();  // lane 0's acquire orders every lane's ring overwrites after the thieves' reads
                     if (tail[q] + pushq[q] - sdone[q] > Q) overflow = true;
                 }
             }

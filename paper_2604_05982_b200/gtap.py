@@ -21,7 +21,7 @@ GTAP_WORKER_BLOCK = 1
 STATUS = {
     0: "GTAP_OK", 1: "GTAP_E_INVAL", 2: "GTAP_E_CUDA", 3: "GTAP_E_NOMEM", 4: "GTAP_E_BUSY",
     5: "GTAP_E_POOL_EXHAUSTED", 6: "GTAP_E_QUEUE_OVERFLOW", 7: "GTAP_E_CHILD_LIMIT",
-    8: "GTAP_E_TIMEOUT", 9: "GTAP_E_BAD_STATE", 10: "GTAP_E_NO_DEVICE", 11: "GTAP_E_UNSUPPORTED",
+    8: "GTAP_E_TIMEOUT", 9: "GTAP_E_BAD_STATE", 10: "GTAP_E_NO_DEVICE", 11: "GTAP_E_UNSUPPORTED", 12: "GTAP_E_INVARIANT",
 }
 
 
@@ -64,7 +64,7 @@ EXPORTS = [
     "gtap_spawn_root", "gtap_reset", "gtap_run", "gtap_sync", "gtap_root_result", "gtap_finalize",
     "gtap_geometry", "gtap_table_destroy", "gtap_table_fib", "gtap_table_fib_cutoff", "gtap_table_nqueens", "gtap_table_nqueens_ex", "gtap_table_tree", "gtap_table_mergesort", "gtap_table_mergesort_ex", "gtap_table_cilksort", "gtap_table_cilksort_ex",
     "gtap_table_spmv",
-    "gtap_table_bfs", "gtap_bfs_init_depth", "gtap_ubench_atomics",
+    "gtap_table_bfs", "gtap_bfs_init_depth", "gtap_ubench_atomics", "gtap_check_read",
 ]
 
 _lib = None
@@ -121,8 +121,10 @@ def lib():
     L.gtap_table_bfs.restype = vp
     L.gtap_bfs_init_depth.argtypes = [vp, u32, i32, vp]
     L.gtap_ubench_atomics.argtypes = [vp, u64, u32, u32, u32, u32, vp, P(ctypes.c_float)]
+    L.gtap_check_read.argtypes = [vp, P(u64), u32]
     for name in ("gtap_config_default", "gtap_init", "gtap_spawn_root", "gtap_reset", "gtap_run", "gtap_sync",
-                 "gtap_root_result", "gtap_finalize", "gtap_geometry", "gtap_ubench_atomics", "gtap_bfs_init_depth"):
+                 "gtap_root_result", "gtap_finalize", "gtap_geometry", "gtap_ubench_atomics", "gtap_bfs_init_depth",
+                 "gtap_check_read"):
         getattr(L, name).restype = ctypes.c_int
     _lib = L
     return L
@@ -319,6 +321,17 @@ class Runtime:
         v = ctypes.c_int64()
         _check(lib().gtap_root_result(self.h, idx, ctypes.byref(v), 8), "gtap_root_result")
         return v.value
+
+    CHECK_FIELDS = ("allocs", "frees", "publications", "dispatches", "suspends", "joins", "continuations",
+                    "v_double_alloc", "v_double_free", "v_double_publish", "v_dispatch_unpublished",
+                    "v_early_resume", "v_join_underflow", "v_suspend_dirty", "_r14", "_r15",
+                    "live_records", "published_unclaimed", "join_counts_open", "outstanding", "roots_left")
+
+    def check_read(self) -> dict:
+        """Scheduler-invariant counters of the last run (GTAP_CHECK build only; else GtapError UNSUPPORTED)."""
+        buf = (ctypes.c_uint64 * 21)()
+        _check(lib().gtap_check_read(self.h, buf, 21), "gtap_check_read")
+        return {k: int(v) for k, v in zip(self.CHECK_FIELDS, buf) if not k.startswith("_")}
 
     def geometry(self, table: Table):
         W, g, b = ctypes.c_uint32(), ctypes.c_uint32(), ctypes.c_uint32()

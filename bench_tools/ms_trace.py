@@ -21,7 +21,7 @@ from paper_2604_05982_b200 import gtap  # noqa: E402
 mode = int(sys.argv[1]) if len(sys.argv) > 1 else 1
 backoff = int(sys.argv[2]) if len(sys.argv) > 2 else bench.MS_CFG["idle_backoff_ns"]
 KIND = {0: "lane merge", 1: "TMA merge", 2: "leaf sort", 3: "warp assist", 4: "block assist", 5: "GPU assist",
-        6: "GPU chunk", 7: "block chunk"}
+        6: "GPU chunk", 7: "block chunk", 8: "chunk split"}
 n = 1 << 24
 keys = synth.keys_int32(n, seed=42, device="cuda")
 scratch = torch.empty_like(keys)

@@ -9,7 +9,7 @@ OUT=gpurun_out/${TAG}_sanitize.txt
 for tool in memcheck racecheck synccheck; do
   for t in fib ms ms0 cs nq spmv bfs tree; do
     log=gpurun_out/${TAG}_san_${tool}_${t}.log
-    timeout -s KILL 900 compute-sanitizer --tool $tool --kernel-name regex:sched_kernel --print-limit 20 \
+    timeout -s KILL 900 compute-sanitizer --tool $tool --kernel-name regex=sched_kernel --print-limit 20 \
         python bench_tools/sanitize_probe.py $t > $log 2>&1
     rc=$?
     summ=$(grep -E "ERROR SUMMARY|RACECHECK SUMMARY|Hazard|ok \(" $log | tr '\n' ' ')

@@ -130,11 +130,6 @@ template <class T>
 struct stats_smem_of<T, decltype((void)T::kStatsSmem, void())> { static constexpr bool value = T::kStatsSmem; };
 
 template <class T, class = void>
-struct assist_all_of { static constexpr bool value = false; };
-template <class T>
-struct assist_all_of<T, decltype((void)T::kAssistAll, void())> { static constexpr bool value = T::kAssistAll; };
-
-template <class T, class = void>
 struct num_queues_of { static constexpr int value = 1; };
 template <class T>
 struct num_queues_of<T, decltype((void)T::kNumQueues, void())> { static constexpr int value = T::kNumQueues; };
@@ -441,15 +436,6 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
             // requesting lanes' join releases below cover every lane's stores.
             uint32_t req = __ballot_sync(0xffffffffu, my != kNone && o.assist != 0u && o.err == 0u);
             const bool any_assist = req != 0u;
-            if constexpr (assist_all_of<T>::value) {
-                // the table takes every request at once (batched assists; it cannot fail)
-                static_assert(kDataWords == 4, "assist_all takes the 4 request words");
-                if (req) {
-                    T::assist_all(args, req, o.ap[0], o.ap[1], o.ap[2], o.ap[3], lane, bx);
-                    if (lane == 0) stat(kStAssist, (uint32_t)__popc(req));
-                    req = 0u;
-                }
-            }
             while (req) {
                 const uint32_t src = (uint32_t)__ffs(req) - 1u;
                 req &= req - 1u;

@@ -20,6 +20,7 @@
 
 #include "table_common.cuh"
 #include "warp_sort.cuh"
+#include "warp_merge.cuh"
 
 namespace gtap {
 
@@ -213,9 +214,6 @@ struct MergeSlot {                           // placed 2 KB-aligned inside the b
 #ifndef GTAP_MS_WR
 #define GTAP_MS_WR 1024
 #endif
-#ifndef GTAP_MS_TILE_BITONIC
-#define GTAP_MS_TILE_BITONIC 1   // warp_merge tiles by a bitonic network (0: merge-path search + serial steps)
-#endif
 constexpr int kWT = GTAP_MS_WT;              // outputs per tile
 constexpr int kVT = kWT / 32;                // outputs per lane per tile
 constexpr int kWR = GTAP_MS_WR;              // keys per ring
@@ -237,8 +235,11 @@ struct MergeSlotHolder {                     // BlockExtra of merge_mode thread:
         return reinterpret_cast<MergeSlot*>(raw + ((2048u - (a & 2047u)) & 2047u));
     }
 };
+static_assert(sizeof(WarpTiles) == sizeof(wm3::WM3Rings), "the two merge cores share the per-warp rings");
 struct WarpAssistHolder {                    // BlockExtra of merge_mode warp: per-warp rings + block board
-    unsigned char raw[sizeof(WarpTiles) * kMsWarps + 128];
+    // per-warp rings, R * 4-aligned (wm3) inside raw; the bulk-copy merge core's buffers and barriers
+    unsigned char raw[sizeof(WarpTiles) * kMsWarps + sizeof(wm3::WM3Rings::ring[0])];
+    wm3::WM3Aux aux[kMsWarps];
     // block assist board (merges >= kBlockAssistMin): one open merge per block
     struct Board {
         uint32_t state;               // 0 free, 1 being set up, 2 open
@@ -247,8 +248,12 @@ struct WarpAssistHolder {                    // BlockExtra of merge_mode warp: p
         uint32_t nchunks, done;
     } board;
     __device__ __forceinline__ WarpTiles* tiles(uint32_t warp) {
+        constexpr uint32_t kAl = sizeof(wm3::WM3Rings::ring[0]);   // one ring: the wrap alignment of wm3
         const uint32_t a = tma::sa(raw);
-        return reinterpret_cast<WarpTiles*>(raw + ((128u - (a & 127u)) & 127u)) + warp;
+        return reinterpret_cast<WarpTiles*>(raw + ((kAl - (a & (kAl - 1u))) & (kAl - 1u))) + warp;
+    }
+    __device__ __forceinline__ wm3::WM3Tiles wtiles(uint32_t warp) {
+        return wm3::WM3Tiles{reinterpret_cast<wm3::WM3Rings*>(tiles(warp)), &aux[warp]};
     }
 };
 
@@ -651,7 +656,6 @@ __device__ __noinline__ void warp_merge(const int32_t* __restrict__ src, int32_t
         wm::wait<1>();  // the window was issued >= 2 tiles ago (see kTopChunk)
         __syncwarp();
         const uint32_t na = min(tile, m - pa), nb = min(tile, r - pb);
-#if GTAP_MS_TILE_BITONIC
         // the tile's kWT outputs by one bitonic half-cleaner + merge network over registers:
         // element e = k * 32 + lane of A[pa, pa + kWT) ++ reverse(B[pb, pb + kWT)) (runs padded with
         // +inf past na / nb); c[e] = min(A[e], B[kWT-1-e]) is bitonic and holds the kWT smallest keys,
@@ -697,93 +701,6 @@ __device__ __noinline__ void warp_merge(const int32_t* __restrict__ src, int32_t
             if (e < tile) dst[out + e] = x[k];
         }
         __syncwarp();                                  // ring reads done before the top-up
-#elif GTAP_MS_TILE_BITONIC == 2
-        // lane k owns outputs [d, d + kVT) of the tile, d = k * kVT: a stable merge-path search at
-        // diagonal d in the rings (4-way, ~4 dependent round trips), then the kVT smallest of
-        // A[ai, ai + kVT) ++ reverse(B[bi, bi + kVT)) by a half-cleaner (A taken iff A <= B: ties
-        // left first) and log2(kVT) in-register compare stages; no shuffles, no serial chain;
-        // 16-B stores when the output is 16-B aligned
-        const uint32_t d = min(lane * (uint32_t)kVT, tile);
-        uint32_t lo = d > nb ? d - nb : 0u, hi = min(d, na);
-        const uint32_t cb = pb + d - 1u;
-        while (lo < hi) {
-            const uint32_t w = hi - lo;
-            const uint32_t q1 = lo + (w >> 2), q2 = lo + (w >> 1), q3 = lo + ((3u * w) >> 2);
-            const bool p1 = RA[(pa + q1) & (kWR - 1u)] <= RB[(cb - q1) & (kWR - 1u)];
-            const bool p2 = RA[(pa + q2) & (kWR - 1u)] <= RB[(cb - q2) & (kWR - 1u)];
-            const bool p3 = RA[(pa + q3) & (kWR - 1u)] <= RB[(cb - q3) & (kWR - 1u)];
-            if (p3)      { lo = q3 + 1u; }
-            else if (p2) { lo = q2 + 1u; hi = q3; }
-            else if (p1) { lo = q1 + 1u; hi = q2; }
-            else         { hi = q1; }
-        }
-        const uint32_t ai = lo, bi = d - lo;
-        const uint32_t cnt = min((uint32_t)kVT, tile - d);
-        int32_t x[kVT];
-        uint32_t ta = 0;
-#pragma unroll
-        for (int v = 0; v < kVT; ++v) {
-            const uint32_t ia = ai + (uint32_t)v, ib = bi + (uint32_t)(kVT - 1 - v);
-            const bool ha = ia < na, hb = ib < nb;
-            const int32_t va = ha ? RA[(pa + ia) & (kWR - 1u)] : INT_MAX;
-            const int32_t vb = hb ? RB[(pb + ib) & (kWR - 1u)] : INT_MAX;
-            const bool takeA = ha && (!hb || va <= vb);
-            x[v] = takeA ? va : vb;
-            ta += takeA ? 1u : 0u;
-        }
-#pragma unroll
-        for (int stride = kVT / 2; stride > 0; stride >>= 1)
-#pragma unroll
-            for (int v = 0; v < kVT; ++v)
-                if ((v & stride) == 0) {
-                    const int32_t u = x[v], w = x[v + stride];
-                    x[v] = min(u, w);
-                    x[v + stride] = max(u, w);
-                }
-        int32_t* o = dst + out + d;
-        if (cnt == (uint32_t)kVT && ((reinterpret_cast<uintptr_t>(o) & 15u) == 0u)) {
-#pragma unroll
-            for (int v = 0; v < kVT; v += 4)
-                *reinterpret_cast<int4*>(o + v) = make_int4(x[v], x[v + 1], x[v + 2], x[v + 3]);
-        } else {
-#pragma unroll
-            for (int v = 0; v < kVT; ++v)
-                if ((uint32_t)v < cnt) o[v] = x[v];
-        }
-        const uint32_t ca = __shfl_sync(0xffffffffu, ai + ta, 31);  // A keys consumed (full tiles)
-        __syncwarp();                                  // ring reads done before the top-up
-#else
-        const uint32_t d = min(lane * (uint32_t)kVT, tile);
-        uint32_t lo = d > nb ? d - nb : 0u, hi = min(d, na);
-        // stable merge-path split at diagonal d: the smallest i in [lo, hi] with !(A[i] <= B[d-1-i]);
-        // three probes per step (4-way), so ~4 dependent shared-memory round trips per tile
-        const uint32_t cb = pb + d - 1u;
-        while (lo < hi) {
-            const uint32_t w = hi - lo;
-            const uint32_t q1 = lo + (w >> 2), q2 = lo + (w >> 1), q3 = lo + ((3u * w) >> 2);
-            const bool p1 = RA[(pa + q1) & (kWR - 1u)] <= RB[(cb - q1) & (kWR - 1u)];
-            const bool p2 = RA[(pa + q2) & (kWR - 1u)] <= RB[(cb - q2) & (kWR - 1u)];
-            const bool p3 = RA[(pa + q3) & (kWR - 1u)] <= RB[(cb - q3) & (kWR - 1u)];
-            if (p3)      { lo = q3 + 1u; }
-            else if (p2) { lo = q2 + 1u; hi = q3; }
-            else if (p1) { lo = q1 + 1u; hi = q2; }
-            else         { hi = q1; }
-        }
-        uint32_t ai = lo, bi = d - lo;
-        const uint32_t cnt = min((uint32_t)kVT, tile - d);
-        int32_t va = RA[(pa + ai) & (kWR - 1u)], vb = RB[(pb + bi) & (kWR - 1u)];
-#pragma unroll
-        for (int v = 0; v < kVT; ++v) {
-            if ((uint32_t)v < cnt) {
-                const bool takeA = bi >= nb || (ai < na && !(vb < va));
-                dst[out + d + v] = takeA ? va : vb;
-                if (takeA) { ++ai; va = RA[(pa + ai) & (kWR - 1u)]; }
-                else       { ++bi; vb = RB[(pb + bi) & (kWR - 1u)]; }
-            }
-        }
-        const uint32_t ca = __shfl_sync(0xffffffffu, ai, (tile - 1u) / (uint32_t)kVT);  // A keys consumed
-        __syncwarp();                                  // ring reads done before the top-up
-#endif
         pa += ca;
         pb += tile - ca;
         out += tile;
@@ -803,6 +720,28 @@ __device__ __noinline__ uint2 warp_split2(const int32_t* src, uint32_t l, uint32
                                           uint32_t t1, uint32_t lane) {
     uint32_t lo0 = t0 > (r - m) ? t0 - (r - m) : 0u, hi0 = min(t0, m - l);
     uint32_t lo1 = t1 > (r - m) ? t1 - (r - m) : 0u, hi1 = min(t1, m - l);
+    {
+        // first round: 32 probes s apart around the proportional guess t * |A| / (|A| + |B|) (a
+        // random merge's split lies within a few sqrt(t) of it); a bracket found there leaves ~s
+        // positions (1-2 further rounds instead of ~4), a miss still halves nothing worse than before
+        const unsigned long long na = m - l, nn = r - l;
+        const uint32_t g0 = (uint32_t)((t0 * na) / nn), g1 = (uint32_t)((t1 * na) / nn);
+        const uint32_t s = max(32u, 1u << ((33u - (uint32_t)__clz(max(t1, 1u))) / 2u)) >> 2;  // ~sqrt(t1) / 4
+        uint32_t q0 = g0 + lane * s, q1 = g1 + lane * s;
+        q0 = q0 >= 15u * s ? q0 - 15u * s : 0u;
+        q1 = q1 >= 15u * s ? q1 - 15u * s : 0u;
+        q0 = min(max(q0, lo0), hi0 > 0u ? hi0 - 1u : 0u);
+        q1 = min(max(q1, lo1), hi1 > 0u ? hi1 - 1u : 0u);
+        const bool a0 = hi0 - lo0 > 32u && __ldcg(src + l + q0) <= __ldcg(src + m + (t0 - q0 - 1u));
+        const bool a1 = hi1 - lo1 > 32u && __ldcg(src + l + q1) <= __ldcg(src + m + (t1 - q1 - 1u));
+        // predicate true below the split, false from it on: the ballot is a prefix of lanes
+        const uint32_t c0 = (uint32_t)__popc(__ballot_sync(0xffffffffu, a0));
+        const uint32_t c1 = (uint32_t)__popc(__ballot_sync(0xffffffffu, a1));
+        const uint32_t ql0 = __shfl_sync(0xffffffffu, q0, (c0 + 31u) & 31u), qh0 = __shfl_sync(0xffffffffu, q0, c0 & 31u);
+        const uint32_t ql1 = __shfl_sync(0xffffffffu, q1, (c1 + 31u) & 31u), qh1 = __shfl_sync(0xffffffffu, q1, c1 & 31u);
+        if (hi0 - lo0 > 32u) { if (c0 > 0u) lo0 = max(lo0, ql0 + 1u); if (c0 < 32u) hi0 = min(hi0, qh0); }
+        if (hi1 - lo1 > 32u) { if (c1 > 0u) lo1 = max(lo1, ql1 + 1u); if (c1 < 32u) hi1 = min(hi1, qh1); }
+    }
     while (hi0 - lo0 > 32u || hi1 - lo1 > 32u) {
         const uint32_t w0 = hi0 - lo0, w1 = hi1 - lo1;
         const uint32_t q0 = lo0 + (uint32_t)(((unsigned long long)(lane + 1u) * w0) / 33u);
@@ -848,50 +787,10 @@ constexpr uint32_t kGSlots = 1024;
 #endif
 constexpr uint32_t kGlobalAssistMin = GTAP_MS_GLOBAL_MIN;
 constexpr uint32_t kGChunk = GTAP_MS_GCHUNK;
-// guided chunking (GTAP_MS_GUIDED): phase p < kGPhases - 1 takes half of the outputs still
-// unassigned (rounded down to its chunk size) in chunks of kGChunk0 >> p keys, the last phase the
-// rest; chunks are claimed in index order, so a slot hands out long chunks first and short ones at
-// its tail (helpers finishing a long chunk late find short ones left). Count and ranges follow from
-// the merge length alone, so the requester and every helper agree without communicating.
-#ifndef GTAP_MS_GUIDED
-#define GTAP_MS_GUIDED 0   // 1: guided chunk sizes (measured no better than uniform chunks at 2^24)
-#endif
-#ifndef GTAP_MS_GC0
-#define GTAP_MS_GC0 8192
-#endif
-#ifndef GTAP_MS_GPH
-#define GTAP_MS_GPH 4
-#endif
-#ifndef GTAP_MS_GUIDED_MIN
-#define GTAP_MS_GUIDED_MIN (1u << 21)   // shorter merges: uniform kGChunk chunks
-#endif
-constexpr uint32_t kGChunk0 = GTAP_MS_GC0;
-constexpr int kGPhases = GTAP_MS_GPH;
-__device__ __forceinline__ uint32_t gch_count(uint32_t n) {
-    if (!GTAP_MS_GUIDED || n < GTAP_MS_GUIDED_MIN) return (n + kGChunk - 1u) / kGChunk;
-    uint32_t b = 0, c = 0;
-#pragma unroll
-    for (int p = 0; p < kGPhases - 1; ++p) {
-        const uint32_t S = kGChunk0 >> p, len = ((n - b) / 2u) / S * S;
-        c += len / S;
-        b += len;
-    }
-    constexpr uint32_t SL = kGChunk0 >> (kGPhases - 1);
-    return c + (n - b + SL - 1u) / SL;
-}
-// output range [x, y) of chunk c (c < gch_count(n))
+// chunk c of an n-key merge: output range [c * kGChunk, min(n, (c + 1) * kGChunk))
+__device__ __forceinline__ uint32_t gch_count(uint32_t n) { return (n + kGChunk - 1u) / kGChunk; }
 __device__ __forceinline__ uint2 gch_range(uint32_t n, uint32_t c) {
-    if (!GTAP_MS_GUIDED || n < GTAP_MS_GUIDED_MIN) return make_uint2(c * kGChunk, min(n, c * kGChunk + kGChunk));
-    uint32_t b = 0;
-#pragma unroll
-    for (int p = 0; p < kGPhases - 1; ++p) {
-        const uint32_t S = kGChunk0 >> p, len = ((n - b) / 2u) / S * S, k = len / S;
-        if (c < k) return make_uint2(b + c * S, b + c * S + S);
-        c -= k;
-        b += len;
-    }
-    constexpr uint32_t SL = kGChunk0 >> (kGPhases - 1);
-    return make_uint2(b + c * SL, min(n, b + c * SL + SL));
+    return make_uint2(c * kGChunk, min(n, c * kGChunk + kGChunk));
 }
 struct __align__(128) GSlot {
     uint32_t state, next, done, nchunks;
@@ -906,6 +805,13 @@ struct GBoard {
     GSlot slot[kGSlots];
 };
 
+// merges up to this many keys run as one bitonic network when the bulk-copy core is available (larger ones:
+// the core); without it, up to kBitonicMax
+#ifndef GTAP_MS_BITONIC_MAX
+#define GTAP_MS_BITONIC_MAX 256
+#endif
+constexpr uint32_t kMsBitonicMax = GTAP_MS_BITONIC_MAX;
+
 #ifndef GTAP_MS_WARP_MINB
 #define GTAP_MS_WARP_MINB 4
 #endif
@@ -916,7 +822,7 @@ struct MsArgs {
     uint32_t cutoff;
     uint32_t n;         // array length (TMA path needs n % 4 == 0 and 16-B aligned buffers)
     uint32_t mode;      // GTAP_MERGE_THREAD (0) or GTAP_MERGE_WARP (1)
-    uint32_t pad;
+    uint32_t bulk;      // 1: n % 4 == 0 and 16-B aligned buffers -> tiled merges by the bulk-copy core (wm3)
     GBoard* gb;         // GPU-wide assist board (table-owned, reset before each run)
 };
 
@@ -945,6 +851,15 @@ struct MergesortTable {
 #endif
     static constexpr uint32_t kAssistMin = GTAP_MS_ASSIST_MIN;
     using Args = MsArgs;
+    // all 32 lanes: stable merge of src[a0, m) and src[b0, r) into dst[o0, ...) by this warp -- the bulk-copy
+    // core (wm3, warp_merge.cuh) when the arrays allow 16-B bulk copies, else the cp.async bitonic tiles
+    __device__ __forceinline__ static void merge_tiles(const Args& a, const int32_t* src, int32_t* dst, uint32_t a0,
+                                                       uint32_t m, uint32_t b0, uint32_t r, uint32_t o0, uint32_t lane,
+                                                       WarpAssistHolder* H) {
+        const uint32_t warp = threadIdx.x >> 5;
+        if (a.bulk) wm3::merge(src, dst, a0, m, b0, r, o0, a.n, lane, H->wtiles(warp));
+        else warp_merge(src, dst, a0, m, b0, r, o0, lane, H->tiles(warp));
+    }
     // warp assist: ap = {l, r, depth}; all 32 lanes
     __device__ __forceinline__ static bool assist(const Args& a, const uint32_t (&ap)[kDataWords], uint32_t lane,
                                                   WarpAssistHolder* H) {
@@ -957,14 +872,13 @@ struct MergesortTable {
             return true;
         }
         const uint32_t m = l + (r - l) / 2u;
-        if (r - l <= kBitonicMax) {
+        if (r - l <= (a.bulk ? kMsBitonicMax : kBitonicMax)) {
             const int32_t* src = buf(a, depth + 1u);
             warp_merge_small(src + l, m - l, src + m, r - m, buf(a, depth) + l, lane);
             MS_TRACE_LANE0(r - l, l, 3u);
             return true;
         }
-        WarpTiles* T = H->tiles(threadIdx.x >> 5);
-        if (r - l >= kGlobalAssistMin && a.gb != nullptr && global_assist(a, l, m, r, depth, lane, T)) {
+        if (r - l >= kGlobalAssistMin && a.gb != nullptr && global_assist(a, l, m, r, depth, lane, H)) {
             MS_TRACE_LANE0(r - l, l, 5u);
             return true;
         }
@@ -984,7 +898,7 @@ struct MergesortTable {
                     B.state = 2u;
                 }
                 __syncwarp();
-                help_chunks(a, H, lane, T);
+                help_chunks(a, H, lane);
                 if (lane == 0) {
                     while (B.done < nch) __nanosleep(128);
                     atomicExch(&H->board.next, 0x80000000u);  // late claims see a closed board
@@ -998,130 +912,13 @@ struct MergesortTable {
                 return true;
             }
         }
-        warp_merge(buf(a, depth + 1u), buf(a, depth), l, m, m, r, l, lane, T);
+        merge_tiles(a, buf(a, depth + 1u), buf(a, depth), l, m, m, r, l, lane, H);
         MS_TRACE_LANE0(r - l, l, 3u);
         return true;
     }
 
-#ifndef GTAP_MS_BATCH
-#define GTAP_MS_BATCH 0   // 1: batched warp assists for leaves <= 128 keys and merges <= 512 keys (measured slower: shuffle-bound)
-#endif
-    static constexpr bool kAssistAll = MODE == 1u && GTAP_MS_BATCH != 0;
-    // gather up to G requests of mask m (consumed) from their lanes: {l, r, depth} per slot, n = 0 if empty
-    template <int G>
-    __device__ __forceinline__ static void take(uint32_t& m, uint32_t a0, uint32_t a1, uint32_t a2,
-                                                uint32_t (&gl)[G], uint32_t (&gr)[G], uint32_t (&gd)[G]) {
-#pragma unroll
-        for (int g = 0; g < G; ++g) {
-            const uint32_t s = m ? (uint32_t)__ffs(m) - 1u : 0u;
-            const uint32_t l = __shfl_sync(0xffffffffu, a0, s), r = __shfl_sync(0xffffffffu, a1, s),
-                           d = __shfl_sync(0xffffffffu, a2, s);
-            gl[g] = l; gr[g] = m ? r : l; gd[g] = d;
-            m &= m - 1u;
-        }
-    }
-    // G merges of <= 32 K keys: src = buf(depth + 1)[l, m) and [m, r) -> buf(depth)[l, r)
-    template <int K, int G>
-    __device__ __noinline__ static uint32_t merge_batch(const Args& a, uint32_t msk, uint32_t a0, uint32_t a1,
-                                                        uint32_t a2, uint32_t lane) {
-        constexpr uint32_t N = 32u * K;
-        {
-            MS_T0;
-            uint32_t gl[G], gr[G], gd[G];
-            take<G>(msk, a0, a1, a2, gl, gr, gd);
-            int32_t x[G][K];
-#pragma unroll
-            for (int g = 0; g < G; ++g) {
-                const uint32_t m = gl[g] + (gr[g] - gl[g]) / 2u, na = m - gl[g], nb = gr[g] - m;
-                const int32_t* src = buf(a, gd[g] + 1u);
-#pragma unroll
-                for (int k = 0; k < K; ++k) {
-                    const uint32_t i = (uint32_t)k * 32u + lane;
-                    x[g][k] = i < na ? src[gl[g] + i] : (i >= N - nb ? src[m + (N - 1u - i)] : INT_MAX);
-                }
-            }
-            warp_bitonic_merge_multi<K, G>(x, lane);
-#pragma unroll
-            for (int g = 0; g < G; ++g) {
-                int32_t* dst = buf(a, gd[g]) + gl[g];
-#pragma unroll
-                for (int k = 0; k < K; ++k) {
-                    const uint32_t i = (uint32_t)k * 32u + lane;
-                    if (i < gr[g] - gl[g]) dst[i] = x[g][k];
-                }
-                MS_TRACE_LANE0(gr[g] - gl[g], gl[g], 3u);
-            }
-        }
-        return msk;
-    }
-    // G leaf sorts of <= 32 K keys: keys[l, r) -> buf(depth)[l, r)
-    template <int K, int G>
-    __device__ __noinline__ static uint32_t leaf_batch(const Args& a, uint32_t msk, uint32_t a0, uint32_t a1,
-                                                       uint32_t a2, uint32_t lane) {
-        {
-            MS_T0;
-            uint32_t gl[G], gr[G], gd[G];
-            take<G>(msk, a0, a1, a2, gl, gr, gd);
-            int32_t x[G][K];
-#pragma unroll
-            for (int g = 0; g < G; ++g)
-#pragma unroll
-                for (int k = 0; k < K; ++k) {
-                    const uint32_t i = (uint32_t)k * 32u + lane;
-                    x[g][k] = i < gr[g] - gl[g] ? a.keys[gl[g] + i] : INT_MAX;
-                }
-            warp_bitonic_sort_multi<K, G>(x, lane);
-#pragma unroll
-            for (int g = 0; g < G; ++g) {
-                int32_t* dst = buf(a, gd[g]) + gl[g];
-#pragma unroll
-                for (int k = 0; k < K; ++k) {
-                    const uint32_t i = (uint32_t)k * 32u + lane;
-                    if (i < gr[g] - gl[g]) dst[i] = x[g][k];
-                }
-                MS_TRACE_LANE0(gr[g] - gl[g], gl[g], 2u);
-            }
-        }
-        return msk;
-    }
-    // scheduler hook (2b), all 32 lanes: every request of mask req (this lane's ap = {l, r, depth, leaf}).
-    // Leaves <= 128 keys go 8 at a time, merges <= 256 / <= 512 keys 4 / 2 at a time (their loads and
-    // network stages interleaved); the rest one at a time through assist().
-    __device__ __noinline__ static void assist_all(const Args& a, uint32_t req, uint32_t a0, uint32_t a1,
-                                                   uint32_t a2, uint32_t a3, uint32_t lane, WarpAssistHolder* H) {
-        const bool mine = (req >> lane) & 1u;
-        const uint32_t n = a1 - a0;
-        const uint32_t mleaf = __ballot_sync(0xffffffffu, mine && a3 == 1u && n <= 128u);
-        const uint32_t m256 = __ballot_sync(0xffffffffu, mine && a3 == 0u && n <= 256u);
-        const uint32_t m512 = __ballot_sync(0xffffffffu, mine && a3 == 0u && n > 256u && n <= 512u);
-        // group sizes follow the request count (an empty slot would still run its network)
-        for (uint32_t m = mleaf; m;) {
-            const int c = __popc(m);
-            m = c >= 8 ? leaf_batch<4, 8>(a, m, a0, a1, a2, lane)
-              : c >= 4 ? leaf_batch<4, 4>(a, m, a0, a1, a2, lane)
-              : c >= 2 ? leaf_batch<4, 2>(a, m, a0, a1, a2, lane)
-                       : leaf_batch<4, 1>(a, m, a0, a1, a2, lane);
-        }
-        for (uint32_t m = m256; m;) {
-            const int c = __popc(m);
-            m = c >= 4 ? merge_batch<8, 4>(a, m, a0, a1, a2, lane)
-              : c >= 2 ? merge_batch<8, 2>(a, m, a0, a1, a2, lane)
-                       : merge_batch<8, 1>(a, m, a0, a1, a2, lane);
-        }
-        for (uint32_t m = m512; m;)
-            m = __popc(m) >= 2 ? merge_batch<16, 2>(a, m, a0, a1, a2, lane) : merge_batch<16, 1>(a, m, a0, a1, a2, lane);
-        uint32_t rest = req & ~(mleaf | m256 | m512);
-        while (rest) {
-            const uint32_t s = (uint32_t)__ffs(rest) - 1u;
-            rest &= rest - 1u;
-            const uint32_t ap[kDataWords] = {__shfl_sync(0xffffffffu, a0, s), __shfl_sync(0xffffffffu, a1, s),
-                                             __shfl_sync(0xffffffffu, a2, s), __shfl_sync(0xffffffffu, a3, s)};
-            assist(a, ap, lane, H);   // mergesort assists always succeed
-        }
-    }
-
     // claim and merge chunks of the block's open board until none is left (all 32 lanes)
-    __device__ __noinline__ static void help_chunks(const Args& a, WarpAssistHolder* H, uint32_t lane, WarpTiles* T) {
+    __device__ __noinline__ static void help_chunks(const Args& a, WarpAssistHolder* H, uint32_t lane) {
         volatile WarpAssistHolder::Board& B = H->board;
         while (true) {
             uint32_t c = 0;
@@ -1136,14 +933,14 @@ struct MergesortTable {
             MS_T0;
             const uint2 sp = warp_split2(src, l, m, r, o0, o1, lane);
             const uint32_t i0 = sp.x, i1 = sp.y;
-            warp_merge(src, buf(a, depth), l + i0, l + i1, m + (o0 - i0), m + (o1 - i1), l + o0, lane, T);
+            merge_tiles(a, src, buf(a, depth), l + i0, l + i1, m + (o0 - i0), m + (o1 - i1), l + o0, lane, H);
             if (lane == 0) atomicAdd(&H->board.done, 1u);  // warp_merge fenced the chunk's stores
             MS_TRACE_LANE0(o1 - o0, l + o0, 7u);
         }
     }
 
     // claim and merge chunks of global slot S until none is left (all 32 lanes)
-    __device__ __noinline__ static void gchunks(const Args& a, GSlot* S, uint32_t lane, WarpTiles* T) {
+    __device__ __noinline__ static void gchunks(const Args& a, GSlot* S, uint32_t lane, WarpAssistHolder* H) {
         using namespace dev;
         const uint32_t si = (uint32_t)(S - a.gb->slot);
         while (true) {
@@ -1168,15 +965,16 @@ struct MergesortTable {
             const uint32_t o0 = orng.x, o1 = orng.y;
             MS_T0;
             const uint2 sp = warp_split2(src, l, m, r, o0, o1, lane);
+            MS_TRACE_LANE0(o1 - o0, l + o0, 8u);   // trace build: the split search alone (kind 8)
             const uint32_t i0 = sp.x, i1 = sp.y;
-            warp_merge(src, buf(a, depth), l + i0, l + i1, m + (o0 - i0), m + (o1 - i1), l + o0, lane, T);
+            merge_tiles(a, src, buf(a, depth), l + i0, l + i1, m + (o0 - i0), m + (o1 - i1), l + o0, lane, H);
             if (lane == 0) atom_add_relaxed(&S->done, 1u);   // warp_merge fenced the chunk's stores
             MS_TRACE_LANE0(o1 - o0, l + o0, 6u);
         }
     }
 
     // find an open global slot with unclaimed chunks and work on it; false if none (all 32 lanes)
-    __device__ __noinline__ static bool help_global_once(const Args& a, uint32_t lane, WarpTiles* T) {
+    __device__ __noinline__ static bool help_global_once(const Args& a, uint32_t lane, WarpAssistHolder* H) {
         using namespace dev;
         GBoard* gb = a.gb;
         uint32_t open = 0, hint = 0;
@@ -1197,13 +995,13 @@ struct MergesortTable {
         const uint32_t rot = (hint + (blockIdx.x * 4u + (threadIdx.x >> 5)) * 7u) & 31u;
         const uint32_t rotw = (wsel >> rot) | (rot ? (wsel << (32u - rot)) : 0u);
         const uint32_t bit = ((uint32_t)__ffs(rotw) - 1u + rot) & 31u;
-        gchunks(a, gb->slot + wix * 32u + bit, lane, T);
+        gchunks(a, gb->slot + wix * 32u + bit, lane, H);
         return true;
     }
 
     // requester side (all 32 lanes); false if no slot was free (the caller merges another way)
     __device__ __noinline__ static bool global_assist(const Args& a, uint32_t l, uint32_t m, uint32_t r,
-                                                      uint32_t depth, uint32_t lane, WarpTiles* T) {
+                                                      uint32_t depth, uint32_t lane, WarpAssistHolder* H) {
         using namespace dev;
         GBoard* gb = a.gb;
         uint32_t sidx = kNone;
@@ -1234,12 +1032,12 @@ struct MergesortTable {
             st_relaxed(&gb->hint, sidx);
         }
         __syncwarp();
-        gchunks(a, S, lane, T);
+        gchunks(a, S, lane, H);
         while (true) {   // wait for the helpers; meanwhile help other open slots
             uint32_t dn = 0;
             if (lane == 0) dn = ld_relaxed(&S->done);
             if (__shfl_sync(0xffffffffu, dn, 0) >= nch) break;
-            if (!help_global_once(a, lane, T) && lane == 0) nanosleep(256);
+            if (!help_global_once(a, lane, H) && lane == 0) nanosleep(256);
             __syncwarp();
         }
         if (lane == 0) {
@@ -1257,13 +1055,13 @@ struct MergesortTable {
     // scheduler hook, idle path (all 32 lanes): help an open GPU-wide assist
     __device__ __forceinline__ static bool help_idle(const Args& a, uint32_t lane, WarpAssistHolder* H) {
         if (a.gb == nullptr) return false;
-        return help_global_once(a, lane, H->tiles(threadIdx.x >> 5));
+        return help_global_once(a, lane, H);
     }
 
     // scheduler hook, top of every cycle (all 32 lanes): join an open board of this block
     __device__ __forceinline__ static void help(const Args& a, uint32_t lane, WarpAssistHolder* H) {
         if (reinterpret_cast<volatile uint32_t&>(H->board.state) == 2u)
-            help_chunks(a, H, lane, H->tiles(threadIdx.x >> 5));
+            help_chunks(a, H, lane);
     }
     using BlockExtra = std::conditional_t<MODE == 1u, WarpAssistHolder, MergeSlotHolder>;
     __device__ __forceinline__ static void block_init(BlockExtra* H) {
@@ -1272,6 +1070,7 @@ struct MergesortTable {
             H->board.next = 0x80000000u;
             H->board.nchunks = 0;
             H->board.done = 0;
+            for (uint32_t w = 0; w < (uint32_t)kMsWarps; ++w) wm3::init_one(&H->aux[w]);
         } else {
             MergeSlot* S = H->slot();
             for (int k = 0; k < 2 * kChains; ++k) {
@@ -1384,7 +1183,8 @@ extern "C" const gtap_task_table* gtap_table_mergesort_ex(int32_t* keys, int32_t
     if (merge_mode > 1u) return nullptr;
     gtap::GBoard* gb = nullptr;
     if (merge_mode == 1u && cudaMalloc(&gb, sizeof(gtap::GBoard)) != cudaSuccess) return nullptr;
-    gtap::MsArgs a{keys, scratch, (uint32_t)cutoff, (uint32_t)n, merge_mode, 0u, gb};
+    const uint32_t bulk = (n % 4u == 0u) && (((uintptr_t)keys | (uintptr_t)scratch) & 15u) == 0u ? 1u : 0u;
+    gtap::MsArgs a{keys, scratch, (uint32_t)cutoff, (uint32_t)n, merge_mode, bulk, gb};
     gtap_task_table* t = merge_mode == 1u
         ? gtap::make_table<gtap::MergesortTable<1u>>("mergesort_warp", a, &gtap::validate_ms)
         : gtap::make_table<gtap::MergesortTable<0u>>("mergesort", a, &gtap::validate_ms);

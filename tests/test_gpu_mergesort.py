@@ -83,7 +83,9 @@ def test_cutoffs(g, rt, mode, cutoff):
 
 
 @pytest.mark.parametrize("kind", ["sorted", "reverse", "equal", "two", "extremes"])
-@pytest.mark.parametrize("n", [100003, 300007])   # 300007: block-assisted top merge (>= 2^17), chunk borders on ties
+# 300007: block-assisted top merge (>= 2^17), chunk borders on ties; 300008 (n % 4 == 0): the same through the
+# bulk-copy merge core
+@pytest.mark.parametrize("n", [100003, 300007, 300008])
 def test_adversarial(g, rt, mode, kind, n):
     rng = np.random.default_rng(7)
     a = {"sorted": np.arange(n), "reverse": np.arange(n, 0, -1), "equal": np.full(n, 3),
@@ -158,12 +160,12 @@ def test_assist_board_saturation(g, nseg, seg):
     assert (st.tasks, st.invocations) == (nseg * tasks, nseg * inv)
 
 
+@pytest.mark.parametrize("n", [(1 << 18) + 77, (1 << 18) + 4])   # cp.async tiles / bulk-copy merge core
 @pytest.mark.parametrize("grid,block", [(1, 32), (3, 128), (148, 64)])
-def test_warp_mode_small_grids(g, grid, block):
+def test_warp_mode_small_grids(g, grid, block, n):
     """merge_mode warp with one warp / few blocks: the block and GPU-wide assists degenerate to the
     requester doing every chunk itself."""
     import torch
-    n = (1 << 18) + 77
     keys = synth.keys_int32(n, seed=5).numpy()
     d = torch.from_numpy(keys).cuda()
     with g.Runtime(g.GTAP_WORKER_THREAD, 0, grid_size=grid, block_size=block, max_tasks_per_worker=4096,

@@ -7,9 +7,7 @@ oracle: the options are alternative implementations of the same task bodies / sc
 
 * GTAP_FSTACK=1, GTAP_FIB_FSTACK=1: a one-entry own free stack, so nearly every surplus free takes
   the overflow path to the home free ring (fib, trees, Cilksort, N-Queens).
-* GTAP_MS_TILE_BITONIC=0 / 2: the merge-path-search tile bodies of the warp merge.
-* GTAP_MS_GUIDED=1, GTAP_MS_BATCH=1, GTAP_LEAF_LANE_MAJOR=1: guided chunks on the GPU-wide board,
-  batched leaf / small-merge assists, lane-major leaf sort.
+* GTAP_MS_VT=23, GTAP_MS_BITONIC_MAX=1024: the bulk-copy merge core with 736-key tiles (default 480) and bitonic merges up to 1024 keys (default 256).
 * GTAP_CS_KARY=0: Cilksort's plain binary split search.
 * GTAP_BFS_POP_BATCH=0 / 32: single pops and the largest batch pop of the block-level leader;
   GTAP_BFS_POP_OLDEST=1 (+ GTAP_BFS_KEEP_CHILD=0): batch pops of the oldest private tasks, with every
@@ -50,7 +48,7 @@ if "tree" in what:
 if "nq" in what:
     c, st = g.nqueens(10, 4, **cfg)
     res["nq10"] = (int(c), st.tasks) == oracle.nqueens(10, 4)
-for name, n in (("ms", 1 << 18), ("ms_ragged", 100003), ("ms_big", 1 << 22)):
+for name, n in (("ms", 1 << 18), ("ms_ragged", 100003), ("ms_big", 1 << 22), ("ms_4k", 300008)):
     if "ms" not in what:
         break
     keys = synth.keys_int32(n, seed=n).numpy()
@@ -92,15 +90,13 @@ def _probe(lib, what):
 
 @pytest.mark.parametrize("defines,what", [
     (("GTAP_FSTACK=1", "GTAP_FIB_FSTACK=1"), "fib tree nq cs"),
-    (("GTAP_MS_TILE_BITONIC=0",), "ms"),
-    (("GTAP_MS_TILE_BITONIC=2",), "ms"),
-    (("GTAP_MS_GUIDED=1", "GTAP_MS_GUIDED_MIN=16384", "GTAP_MS_BATCH=1", "GTAP_LEAF_LANE_MAJOR=1"), "ms"),
+    (("GTAP_MS_VT=23", "GTAP_MS_BITONIC_MAX=1024"), "ms"),
     (("GTAP_CS_KARY=0",), "cs"),
     (("GTAP_BFS_POP_BATCH=0",), "bfs"),
     (("GTAP_BFS_POP_BATCH=32",), "bfs"),
     (("GTAP_BFS_POP_OLDEST=1",), "bfs"),
     (("GTAP_BFS_POP_OLDEST=1", "GTAP_BFS_KEEP_CHILD=0"), "bfs"),
-], ids=["fstack1", "tile_search", "tile_search_inreg", "guided_batch_lanemajor", "cs_binary_split", "bfs_pop1",
+], ids=["fstack1", "ms_vt23_bitonic1024", "cs_binary_split", "bfs_pop1",
         "bfs_pop32", "bfs_pop_oldest", "bfs_pop_oldest_nokeep"])
 def test_variant_parity(cuda_device, defines, what):
     lib = _variant(defines)

@@ -294,6 +294,15 @@ const gtap_task_table *gtap_table_spmv(const int32_t *row_ptr, const int32_t *co
 const gtap_task_table *gtap_table_bfs(const int32_t *row_ptr, const int32_t *col,
                                       int32_t *depth, uint32_t nv);
 
+/* BFS with a choice of owner pop order (a B200 scheduling option, semantics-free: the levels are the
+ * same): order 0 = gtap_table_bfs (LIFO pops of the own deque, the block keeps its newest child,
+ * P:89-93); order 1 = oldest-first batch pops, every child pushed -- the deques behave FIFO, closer to
+ * level order, fewer re-expansions, but each deque may hold a whole local frontier (size
+ * max_tasks_per_worker / queue_capacity accordingly; an undersized ring fails the run with
+ * GTAP_E_QUEUE_OVERFLOW). NULL on bad arguments or order > 1. */
+const gtap_task_table *gtap_table_bfs_ex(const int32_t *row_ptr, const int32_t *col,
+                                         int32_t *depth, uint32_t nv, uint32_t order);
+
 /* BFS input preparation (reading R18): depth[v] = INT32_MAX for v != src,
  * depth[src] = 0, asynchronously on `stream`. */
 gtap_status gtap_bfs_init_depth(int32_t *depth, uint32_t nv, int32_t src, void *stream);

@@ -25,6 +25,7 @@
 namespace gtap {
 
 constexpr uint32_t kNone = 0xFFFFFFFFu;
+constexpr uint32_t kExit = 0xFFFFFFFEu;   // block scheduler: the cycle's task word when the block leaves
 constexpr uint32_t kRootFlag = 0x80000000u;
 constexpr int kDataWords = 4;  // 16-B payload per record (GTAP_MAX_TASK_DATA_SIZE default)
 

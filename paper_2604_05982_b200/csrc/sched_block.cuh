@@ -50,8 +50,9 @@ struct ChildSpec {
 
 template <class T>
 struct BlockSmem {
-    uint32_t task_id;         // task of this cycle (kNone: none)
-    uint32_t exit_flag;
+    // task of a cycle (kNone: none, kExit: leave), double-buffered by cycle parity: warp 0 writes the next
+    // cycle's word while the other warps may still read this cycle's (an idle cycle has no second barrier)
+    uint32_t task_id[2];
     uint32_t fn, state, parent, ord;
     uint32_t d[kDataWords];
     uint32_t nspawn;          // staged children (smem atomic)
@@ -300,7 +301,8 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) block_sched_ker
         if (lane == 0) L.st[ST_TASKS] += mine;
         __syncwarp();
     }
-    if (tid == 0) { sm.exit_flag = 0; sm.nfree = 0; sm.kept_fresh = 0; }
+    if (tid == 0) { sm.nfree = 0; sm.kept_fresh = 0; }
+    uint32_t par = 0;   // cycle parity (every thread passes the acquire barrier once per cycle)
     __syncthreads();
 
     while (true) {
@@ -458,17 +460,18 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) block_sched_ker
                     if (!d && p.watchdog_ns && globaltimer() - t0 > p.watchdog_ns) raise_error(p.ctl, GTAP_E_TIMEOUT);
                 }
                 d = __shfl_sync(0xffffffffu, d, 0);
-                if (d && lane == 0) sm.exit_flag = 1;
+                if (d) id = kExit;
                 if (!d) {
                     nanosleep(L.backoff);
                     L.backoff = min(L.backoff * 2u, p.idle_backoff);
                 }
             }
-            if (lane == 0) sm.task_id = id;
+            if (lane == 0) sm.task_id[par] = id;
         }
         __syncthreads();
-        if (sm.exit_flag) break;
-        const uint32_t my = sm.task_id;
+        const uint32_t my = sm.task_id[par];
+        par ^= 1u;
+        if (my == kExit) break;
         if (my == kNone) continue;
 
         // ================= all threads: run the task body =================

@@ -14,6 +14,18 @@
 
 namespace gtap {
 
+// ORDER 0: the paper's owner order (LIFO pops of the own deque; the block keeps its newest child);
+// ORDER 1: oldest-first batch pops and every child pushed (the deques behave FIFO, closer to level order:
+// RMAT-22 x 16 sources 9.4 -> 8.4 ms, expansions per reached vertex 2.0 -> 1.7), at the price of deques that
+// hold a frontier (size max_tasks_per_worker / queue_capacity for it)
+struct BfsArgs {
+    const int32_t* row_ptr;
+    const int32_t* col;
+    int32_t* depth;
+    uint32_t nv;
+    uint32_t pad;
+};
+template <uint32_t ORDER>
 struct BfsTable {
     static constexpr uint32_t kKind = GTAP_WORKER_BLOCK;
     static constexpr int kMaxChildren = 0;  // dynamic (no taskwait: no join metadata)
@@ -33,27 +45,15 @@ struct BfsTable {
 #define GTAP_BFS_POP_BATCH 4
 #endif
     static constexpr int kPopBatch = GTAP_BFS_POP_BATCH;  // sched_block.cuh batch pop
-#ifndef GTAP_BFS_POP_OLDEST
-#define GTAP_BFS_POP_OLDEST 0
+    static constexpr bool kPopOldest = ORDER == 1u;
+    static constexpr bool kKeepChild = ORDER == 0u;
+#ifndef GTAP_BFS_SKIP_STALE
+#define GTAP_BFS_SKIP_STALE 0   // 1: a task whose vertex improved since its spawn returns at once (measured slower)
 #endif
-    // 1: batch pops take the oldest private tasks (closer to level order: 4.83 -> 4.37 M tasks, 8.9 -> 8.4 ms),
-    // but a deque then behaves FIFO and holds a frontier: with small queue capacities (4096 per worker,
-    // RMAT-16) runs hit GTAP_E_QUEUE_OVERFLOW that the LIFO order never reaches, so it is off by default
-    static constexpr bool kPopOldest = GTAP_BFS_POP_OLDEST != 0;
-#ifndef GTAP_BFS_KEEP_CHILD
-#define GTAP_BFS_KEEP_CHILD 1   // 0: every child to the deque (8.3-8.6 -> 8.1-8.2 ms with oldest-first pops, but see kPopOldest)
-#endif
-    static constexpr bool kKeepChild = GTAP_BFS_KEEP_CHILD != 0;
     struct Scratch {
         uint32_t unused;
     };
-    struct Args {
-        const int32_t* row_ptr;
-        const int32_t* col;
-        int32_t* depth;
-        uint32_t nv;
-        uint32_t pad;
-    };
+    using Args = BfsArgs;
     template <class Ctx>
     __device__ __forceinline__ static void exec_block(const Args& a, Ctx& ctx, uint32_t fn, uint32_t state,
                                                       const uint32_t (&d)[kDataWords]) {
@@ -63,6 +63,14 @@ struct BfsTable {
         }
         const uint32_t v = d[0];
         const int32_t dv = dev::ld_relaxed(&a.depth[v]);
+#if GTAP_BFS_SKIP_STALE
+        // d[1] = the depth v had when this task was spawned; a smaller depth now means a later improvement
+        // spawned a newer task for v, which will expand it with that depth: this one has nothing to add
+        if (dv < (int32_t)d[1]) {
+            if (threadIdx.x == 0) ctx.finish_void();
+            return;
+        }
+#endif
         const int32_t s = __ldg(&a.row_ptr[v]), e = __ldg(&a.row_ptr[v + 1]);
         const int32_t nd = dv + 1;
         const uint32_t bd = blockDim.x;
@@ -85,7 +93,7 @@ struct BfsTable {
             for (int j = 0; j < kU; ++j) old[j] = u[j] >= 0 ? atomicMin(&a.depth[u[j]], nd) : nd;
 #pragma unroll
             for (int j = 0; j < kU; ++j)
-                if (old[j] > nd) ctx.spawn(0u, (uint32_t)u[j]);
+                if (old[j] > nd) ctx.spawn(0u, (uint32_t)u[j], (uint32_t)nd);   // P:1063-1065 (d[1]: spawn depth)
             if (++k == chunk_every) {                               // uniform
                 k = 0;
                 if (base + (int32_t)step < e) ctx.flush(chunk_every * step);
@@ -96,18 +104,24 @@ struct BfsTable {
 };
 
 static int validate_bfs(const gtap_task_table* t, uint32_t fn, const uint32_t* d) {
-    BfsTable::Args a;
+    BfsArgs a;
     std::memcpy(&a, t->args, sizeof(a));
     return (fn == 0u && d[0] < a.nv) ? 0 : -1;
 }
 
 }  // namespace gtap
 
+extern "C" const gtap_task_table* gtap_table_bfs_ex(const int32_t* row_ptr, const int32_t* col, int32_t* depth,
+                                                    uint32_t nv, uint32_t order) {
+    if (!row_ptr || !col || !depth || nv == 0 || order > 1u) return nullptr;
+    gtap::BfsArgs a{row_ptr, col, depth, nv, 0u};
+    return order == 0u ? gtap::make_table<gtap::BfsTable<0>>("bfs", a, &gtap::validate_bfs)
+                       : gtap::make_table<gtap::BfsTable<1>>("bfs_fifo", a, &gtap::validate_bfs);
+}
+
 extern "C" const gtap_task_table* gtap_table_bfs(const int32_t* row_ptr, const int32_t* col, int32_t* depth,
                                                  uint32_t nv) {
-    if (!row_ptr || !col || !depth || nv == 0) return nullptr;
-    gtap::BfsTable::Args a{row_ptr, col, depth, nv, 0u};
-    return gtap::make_table<gtap::BfsTable>("bfs", a, &gtap::validate_bfs);
+    return gtap_table_bfs_ex(row_ptr, col, depth, nv, 0u);
 }
 
 namespace {

@@ -45,8 +45,8 @@ def csr_from_edges(nv, edges):
     return torch.tensor(rp, dtype=torch.int32), torch.tensor(col if col else [0], dtype=torch.int32)
 
 
-def check(g, rt, rp, col, src):
-    depth, st = g.bfs(rp.cuda(), col.cuda(), src, rt=rt)
+def check(g, rt, rp, col, src, order=0):
+    depth, st = g.bfs(rp.cuda(), col.cuda(), src, rt=rt, order=order)
     ref = oracle.bfs(rp, col[: int(rp[-1])] if int(rp[-1]) else col, src)
     assert np.array_equal(depth.cpu().numpy(), ref)
     reached = int((ref != oracle.INT32_MAX).sum())
@@ -97,12 +97,13 @@ def test_hub_capacity_error(g):
         assert e.value.code in (5, 6)
 
 
-def test_full_size_config4(g):
+@pytest.mark.parametrize("order", [0, 1])
+def test_full_size_config4(g, order):
     import bench
     rp, col = synth.rmat_csr(22, 16, seed=3, device="cuda")
     src = synth.bfs_sources(rp, 1, seed=5)[0]
     with g.Runtime(g.GTAP_WORKER_BLOCK, 0, watchdog_ns=60_000_000_000, **bench.BFS_CFG) as r:
-        depth, st = g.bfs(rp, col, src, rt=r)
+        depth, st = g.bfs(rp, col, src, rt=r, order=order)
     ref = oracle.bfs(rp.cpu(), col.cpu(), src)
     assert np.array_equal(depth.cpu().numpy(), ref)
 
@@ -115,3 +116,27 @@ def test_batch_steal(g, steal_max):
                    steal_max=steal_max, watchdog_ns=WD) as r:
         for s in synth.bfs_sources(rp, 3, seed=steal_max):
             check(g, r, rp, col, s)
+
+
+@pytest.mark.parametrize("scale", [10, 14, 16])
+def test_rmat_fifo_order(g, scale):
+    """gtap_table_bfs_ex order 1 (oldest-first pops, every child pushed): same levels; deques sized for a
+    local frontier."""
+    rp, col = synth.rmat_csr(scale, 16, seed=scale)
+    with g.Runtime(g.GTAP_WORKER_BLOCK, 0, grid_size=148 * 2, block_size=128, max_tasks_per_worker=1 << 16,
+                   watchdog_ns=WD) as r:
+        for s in synth.bfs_sources(rp, 3, seed=scale):
+            check(g, r, rp, col, s, order=1)
+        check(g, r, *csr_from_edges(300, [(i, i + 1) for i in range(299)]), 0, order=1)   # path
+        check(g, r, *csr_from_edges(50, [(1, 2), (3, 4)]), 0, order=1)                    # isolated source
+
+
+def test_fifo_order_overflow_fails_loudly(g):
+    """order 1 holds frontiers in the deques: an undersized ring must fail with an error, not hang."""
+    rp, col = synth.rmat_csr(16, 16, seed=16)
+    src = synth.bfs_sources(rp, 1, seed=16)[0]
+    with g.Runtime(g.GTAP_WORKER_BLOCK, 0, grid_size=2, block_size=64, max_tasks_per_worker=64,
+                   watchdog_ns=WD) as r:
+        with pytest.raises(g.GtapError) as e:
+            check(g, r, rp, col, src, order=1)
+        assert e.value.code in (5, 6)

@@ -10,8 +10,7 @@ oracle: the options are alternative implementations of the same task bodies / sc
 * GTAP_MS_VT=23, GTAP_MS_BITONIC_MAX=1024: the bulk-copy merge core with 736-key tiles (default 480) and bitonic merges up to 1024 keys (default 256).
 * GTAP_CS_KARY=0: Cilksort's plain binary split search.
 * GTAP_BFS_POP_BATCH=0 / 32: single pops and the largest batch pop of the block-level leader;
-  GTAP_BFS_POP_OLDEST=1 (+ GTAP_BFS_KEEP_CHILD=0): batch pops of the oldest private tasks, with every
-  child pushed instead of the newest kept for the block's next task.
+  GTAP_BFS_SKIP_STALE=1: a task whose vertex improved since its spawn returns at once (measured slower).
 """
 import json
 import os
@@ -61,9 +60,10 @@ if "bfs" in what:
     rp, col = synth.rmat_csr(14, 16, seed=4)
     src = synth.bfs_sources(rp, 1, seed=4)[0]
     for grid, block in ((148, 64), (1, 32)):
-        depth, st = g.bfs(rp.cuda(), col.cuda(), src, grid_size=grid, block_size=block, max_tasks_per_worker=1 << 16,
-                          steal_max=32, watchdog_ns=60_000_000_000)
-        res[f"bfs{grid}"] = bool(np.array_equal(depth.cpu().numpy(), oracle.bfs(rp, col, src)))
+        for order in (0, 1):
+            depth, st = g.bfs(rp.cuda(), col.cuda(), src, grid_size=grid, block_size=block,
+                              max_tasks_per_worker=1 << 16, steal_max=32, watchdog_ns=60_000_000_000, order=order)
+            res[f"bfs{grid}_{order}"] = bool(np.array_equal(depth.cpu().numpy(), oracle.bfs(rp, col, src)))
 if "cs" in what:
     keys = synth.keys_int32(300007, seed=5).numpy()
     d = torch.from_numpy(keys).cuda()
@@ -94,10 +94,9 @@ def _probe(lib, what):
     (("GTAP_CS_KARY=0",), "cs"),
     (("GTAP_BFS_POP_BATCH=0",), "bfs"),
     (("GTAP_BFS_POP_BATCH=32",), "bfs"),
-    (("GTAP_BFS_POP_OLDEST=1",), "bfs"),
-    (("GTAP_BFS_POP_OLDEST=1", "GTAP_BFS_KEEP_CHILD=0"), "bfs"),
+    (("GTAP_BFS_SKIP_STALE=1",), "bfs"),
 ], ids=["fstack1", "ms_vt23_bitonic1024", "cs_binary_split", "bfs_pop1",
-        "bfs_pop32", "bfs_pop_oldest", "bfs_pop_oldest_nokeep"])
+        "bfs_pop32", "bfs_skip_stale"])
 def test_variant_parity(cuda_device, defines, what):
     lib = _variant(defines)
     res = _probe(lib, what)

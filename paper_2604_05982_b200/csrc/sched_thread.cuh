@@ -208,26 +208,31 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
     uint32_t nkept = 0;
     uint32_t rng = hash32(p.seed * 0x9E3779B97F4A7C15ull + (unsigned long long)w * 32u + lane);
     uint32_t backoff = 32;
-    // per-warp statistics (lane 0 counts): registers by default; tables with kStatsSmem keep them in
-    // shared memory (12 x 64-bit counters held across the loop cost 24 registers per thread; the
-    // mergesort kernel at its 128-register cap spilled 188 B without them there; fib is 3 % faster
-    // with registers)
+    // per-warp statistics (lane 0 counts): 32-bit registers folded into the warp's 64-bit shared-memory
+    // counters every 2^16 loop iterations (at most 2^7 per counter per iteration: no overflow) and at exit;
+    // tables with kStatsSmem add straight into shared memory (12 register counters cost the mergesort
+    // kernel spills at its 128-register cap)
     constexpr bool kStSmem = stats_smem_of<T>::value;
     enum { kStTasks, kStInv, kStPops, kStKept, kStSok, kStSfail, kStStolen, kStPush, kStCyc, kStIdle, kStRfree,
            kStAssist, kStN };
-    unsigned long long streg[kStSmem ? 1 : kStN];
+    uint32_t streg[kStSmem ? 1 : kStN];
 #pragma unroll
-    for (int k = 0; k < (kStSmem ? 1 : kStN); ++k) streg[k] = 0ull;
-    if (kStSmem && lane < (uint32_t)kStN) sm.st[lane] = 0ull;
+    for (int k = 0; k < (kStSmem ? 1 : kStN); ++k) streg[k] = 0u;
+    if (lane < (uint32_t)kStN) sm.st[lane] = 0ull;
     __syncwarp();
-    auto stat = [&](int k, unsigned long long v) {
-        if constexpr (kStSmem) atomicAdd(&sm.st[k], v); else streg[k] += v;
+    auto stat = [&](int k, uint32_t v) {
+        if constexpr (kStSmem) atomicAdd(&sm.st[k], (unsigned long long)v); else streg[k] += v;
     };
-    auto stget = [&](int k) -> unsigned long long {
-        if constexpr (kStSmem) return sm.st[k]; else return streg[k];
+    auto stflush = [&]() {   // lane 0
+        if constexpr (!kStSmem) {
+#pragma unroll
+            for (int k = 0; k < kStN; ++k) { sm.st[k] += streg[k]; streg[k] = 0u; }
+        }
     };
+    auto stget = [&](int k) -> unsigned long long { return sm.st[k]; };
     const unsigned long long t0 = globaltimer();
-    uint32_t cyc_u = 0;  // warp-uniform cycle counter (every lane increments it)
+    const bool wd_on = p.watchdog_ns != 0ull;
+    uint32_t cyc_u = 0;  // warp-uniform loop-iteration counter (statistics flush, watchdog)
     bool failed = false;
 
     // ---- entry: roots r = w, w + W, ... go to this warp's queue 0
@@ -255,6 +260,7 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
     }
 
     while (true) {
+        if (((++cyc_u) & 0xFFFFu) == 0u && lane == 0) stflush();
         if constexpr (assist_of<T>::value) T::help(args, lane, bx);  // join the block's open assist, if any
         // ================= (1) acquire =================
         uint32_t n = nkept;
@@ -772,7 +778,7 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
         }
         __syncwarp();
         if (done_seen) break;  // error raised elsewhere (completion implies no tasks left)
-        if (p.watchdog_ns && ((++cyc_u) & 4095u) == 0u) {
+        if ((cyc_u & 4095u) == 0u && wd_on) {
             uint32_t tmo = 0;
             if (lane == 0 && globaltimer() - t0 > p.watchdog_ns) { raise_error(p.ctl, GTAP_E_TIMEOUT); tmo = 1; }
             if (__shfl_sync(0xffffffffu, tmo, 0)) break;
@@ -781,6 +787,7 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
 
     // ---- exit: fold per-warp counters into the control block
     if (lane == 0) {
+        stflush();
         unsigned long long* s = p.ctl->stats;
         atomicAdd(&s[ST_TASKS], stget(kStTasks));
         atomicAdd(&s[ST_INVOC], stget(kStInv));

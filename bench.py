@@ -476,21 +476,31 @@ def bench_fib_forest(dev, ws=1, rank=0, reps=3):
                 scaling="strong")
 
 
-def bench_epaq(dev, cutoff=10, reps=3):
-    """SURVEY §8(f) NEXT #1: fib(40) with cutoff 10, 1 queue vs EPAQ with 3 queues (P:788-789)."""
+EPAQ_POOL = 32768   # records per worker: the "stay" policy holds a deeper frontier of suspended tasks
+
+
+def bench_epaq(dev, reps=3):
+    """SURVEY §8(f) NEXT #1: fib(40) with a cutoff, 1 queue vs EPAQ with 3 queues (P:788-789), under both
+    kept-class policies (gtap_config.queue_policy: 0 rotate every cycle, 1 stay while the class has work,
+    P:177-178 literal), at cutoff 10 (SURVEY) and 14; every run with EPAQ_POOL records per worker."""
     import paper_2604_05982_b200 as g
     out = {}
-    for nq in (1, 3):
-        with g.Runtime(g.GTAP_WORKER_THREAD, dev.index, num_queues=3, **FIB_CFG) as rt:
-            ms = []
-            for i in range(reps + 1):
-                v, st = g.fib_cutoff(FIB_N, cutoff, nq, rt=rt)
-                assert v == _fib_value(FIB_N)
-                if i:
-                    ms.append(st.device_ms)
-        out[nq] = (statistics.median(ms), st.tasks)
-    return dict(workload=f"fib(40) cutoff {cutoff}: EPAQ 3 queues vs 1 queue (NEXT #1)", metric="speedup",
-                value=out[1][0] / out[3][0], ms_1q=out[1][0], ms_3q=out[3][0], tasks=out[3][1],
+    for cutoff in (10, 14):
+        for nq, pol in ((1, 0), (3, 0), (3, 1)):
+            with g.Runtime(g.GTAP_WORKER_THREAD, dev.index, num_queues=3, queue_policy=pol,
+                           **dict(FIB_CFG, max_tasks_per_worker=EPAQ_POOL)) as rt:
+                ms = []
+                for i in range(reps + 1):
+                    v, st = g.fib_cutoff(FIB_N, cutoff, nq, rt=rt)
+                    assert v == _fib_value(FIB_N)
+                    if i:
+                        ms.append(st.device_ms)
+            out[(cutoff, nq, pol)] = statistics.median(ms)
+    pts = {f"cutoff{c}": dict(ms_1q=out[(c, 1, 0)], ms_epaq_rotate=out[(c, 3, 0)], ms_epaq_stay=out[(c, 3, 1)],
+                              speedup_rotate=out[(c, 1, 0)] / out[(c, 3, 0)],
+                              speedup_stay=out[(c, 1, 0)] / out[(c, 3, 1)]) for c in (10, 14)}
+    return dict(workload="fib(40) with cutoff: EPAQ 3 queues vs 1 queue (NEXT #1)", metric="speedup",
+                value=pts["cutoff10"]["speedup_stay"], points=pts, records_per_worker=EPAQ_POOL,
                 paper="~1.8x on GH200 (P:788)")
 
 

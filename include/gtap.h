@@ -86,7 +86,10 @@ typedef struct {
     uint64_t seed;                 /* victim-selection PRNG seed */
     uint64_t watchdog_ns;          /* 0 = off; else a run longer than this fails with GTAP_E_TIMEOUT */
     uint32_t idle_backoff_ns;      /* cap of an idle worker's exponential nanosleep backoff; 0 = 8192 */
-    uint32_t reserved1;
+    uint32_t queue_policy;         /* EPAQ (num_queues > 1) class kept for a warp's next cycle:
+                                      0 = the next queue in round-robin order every cycle (DESIGN R24);
+                                      1 = stay on the queue in use while the cycle produced runnable tasks
+                                      of it, else the next one (round robin) that has some */
 } gtap_config;
 
 typedef struct gtap_runtime gtap_runtime;

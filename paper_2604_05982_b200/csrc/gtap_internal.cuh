@@ -130,7 +130,7 @@ struct KParams {
     uint32_t max_child;      // GTAP_MAX_CHILD_TASKS (runtime check)
     uint32_t idle_backoff;   // max idle nanosleep (ns)
     uint32_t nq;             // deques per worker in the workspace (GTAP_NUM_QUEUES, EPAQ)
-    uint32_t pad2;
+    uint32_t qpolicy;        // EPAQ kept-class choice: 0 rotate every cycle, 1 stay while the class has work
     unsigned long long seed;
     unsigned long long watchdog_ns;
     TaskRec* rec;            // W << logM records

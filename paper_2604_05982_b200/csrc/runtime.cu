@@ -79,6 +79,7 @@ gtap_status resolve(const gtap_config* in, gtap_config* c, int sm_count) {
     if (c->max_roots == 0) c->max_roots = 65536;
     if (c->idle_backoff_ns == 0) c->idle_backoff_ns = 8192;
     if (c->idle_backoff_ns < 32 || c->idle_backoff_ns > 1000000) return GTAP_E_INVAL;
+    if (c->queue_policy > 1) return GTAP_E_INVAL;
     const uint32_t wpb = (c->worker_kind == GTAP_WORKER_THREAD) ? c->block_size / 32 : 1;
     uint64_t W;
     if (c->grid_size) W = (uint64_t)c->grid_size * wpb;
@@ -360,6 +361,7 @@ static gtap_status run_impl(gtap_runtime* rt, cudaStream_t s) {
     p.watchdog_ns = rt->cfg.watchdog_ns;
     p.idle_backoff = rt->cfg.idle_backoff_ns;
     p.nq = rt->cfg.num_queues;
+    p.qpolicy = rt->cfg.queue_policy;
     p.rec = reinterpret_cast<gtap::TaskRec*>(rt->ws + rt->L.rec);
     p.ring = reinterpret_cast<uint32_t*>(rt->ws + rt->L.ring);
     p.dq = reinterpret_cast<gtap::DequeMeta*>(rt->ws + rt->L.dq);

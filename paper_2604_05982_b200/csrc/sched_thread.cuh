@@ -685,7 +685,27 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
             // EPAQ: the class of the next cycle is the next queue in round-robin order;
             // the kept set holds this cycle's new tasks of that class, so every class -- including
             // continuations, which free records -- is visited every NQ cycles
-            const uint32_t qk = NQ > 1 ? (qc + 1u) % (uint32_t)NQ : 0u;
+            uint32_t qk = NQ > 1 ? (qc + 1u) % (uint32_t)NQ : 0u;
+            if (NQ > 1 && p.qpolicy == 1u) {
+                // P:177-178 read literally: stay on the class in use while this cycle produced runnable tasks
+                // of it, else the next class (round robin from it) that did
+                uint32_t has = 0;
+                for (uint32_t base = 0; base < R; base += 32) {
+                    const uint32_t i = base + lane;
+                    uint32_t id = kNone, qi = 0;
+                    if (i < R) {
+                        id = (i < P) ? sm.pbuf[i] : sm.cbuf[i - P];
+                        qi = (i < P) ? sm.pqb[i] : sm.cqb[i - P];
+                    }
+                    has |= __reduce_or_sync(0xffffffffu, (i < R && !(id & kHeavyBit)) ? 1u << qi : 0u);
+                }
+                qk = qc;
+#pragma unroll
+                for (int k = 0; k < NQ; ++k) {
+                    const uint32_t q = (qc + (uint32_t)k) % (uint32_t)NQ;
+                    if ((has >> q) & 1u) { qk = q; break; }
+                }
+            }
             // pass 1: count pushes per queue (capacity check before any ring write)
             for (uint32_t base = 0; base < R; base += 32) {
                 const uint32_t i = base + lane;

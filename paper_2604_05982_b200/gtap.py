@@ -40,7 +40,7 @@ class Config(ctypes.Structure):
         ("max_task_data_size", ctypes.c_uint32), ("assume_no_taskwait", ctypes.c_uint32),
         ("steal_attempts", ctypes.c_uint32), ("steal_max", ctypes.c_uint32), ("max_roots", ctypes.c_uint32),
         ("seed", ctypes.c_uint64), ("watchdog_ns", ctypes.c_uint64),
-        ("idle_backoff_ns", ctypes.c_uint32), ("reserved1", ctypes.c_uint32),
+        ("idle_backoff_ns", ctypes.c_uint32), ("queue_policy", ctypes.c_uint32),
     ]
 
 
@@ -270,7 +270,7 @@ class Runtime:
     def __init__(self, kind: int, device: int = 0, *, grid_size: int = 0, block_size: int = 0,
                  max_tasks_per_worker: int = 0, queue_capacity: int = 0, steal_attempts: int = 0,
                  steal_max: int = 0, seed: int = 0x5EED, watchdog_ns: int = 0, max_roots: int = 0,
-                 idle_backoff_ns: int = 0, num_queues: int = 0, max_child_tasks: int = 0,
+                 idle_backoff_ns: int = 0, num_queues: int = 0, max_child_tasks: int = 0, queue_policy: int = 0,
                  torch_workspace: bool = True):
         import torch
         L = lib()
@@ -279,7 +279,7 @@ class Runtime:
         for k, v in dict(grid_size=grid_size, block_size=block_size, max_tasks_per_worker=max_tasks_per_worker,
                          queue_capacity=queue_capacity, steal_attempts=steal_attempts, steal_max=steal_max,
                          watchdog_ns=watchdog_ns, max_roots=max_roots, idle_backoff_ns=idle_backoff_ns,
-                         num_queues=num_queues, max_child_tasks=max_child_tasks).items():
+                         num_queues=num_queues, max_child_tasks=max_child_tasks, queue_policy=queue_policy).items():
             if v:
                 setattr(cfg, k, v)
         cfg.seed = seed

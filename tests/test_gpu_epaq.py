@@ -59,3 +59,20 @@ def test_fib40_cutoff10_epaq(g):
         for nq in (1, 3):
             v, st = g.fib_cutoff(40, 10, nq, rt=r)
             assert (v, st.tasks, st.invocations) == ref
+
+
+@pytest.mark.parametrize("cutoff", [0, 5, 10])
+@pytest.mark.parametrize("n", [2, 11, 20, 27])
+def test_queue_policy_stay_parity(g, cutoff, n):
+    """queue_policy 1 (stay on the class in use while it has runnable tasks, P:177-178 literal) is
+    semantics-free too."""
+    with g.Runtime(g.GTAP_WORKER_THREAD, 0, grid_size=148 * 4, block_size=128, max_tasks_per_worker=4096,
+                   num_queues=3, queue_policy=1, watchdog_ns=WD) as r:
+        v, st = g.fib_cutoff(n, cutoff, 3, rt=r)
+    ov, tasks, inv, _ = oracle.fib_cutoff(n, cutoff)
+    assert (v, st.tasks, st.invocations) == (ov, tasks, inv)
+
+
+def test_queue_policy_range(g):
+    with pytest.raises(g.GtapError):
+        g.Runtime(g.GTAP_WORKER_THREAD, 0, num_queues=3, queue_policy=2)

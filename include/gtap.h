@@ -90,6 +90,11 @@ typedef struct {
                                       0 = the next queue in round-robin order every cycle (DESIGN R24);
                                       1 = stay on the queue in use while the cycle produced runnable tasks
                                       of it, else the next one (round robin) that has some */
+    uint32_t victim_policy;        /* steal-victim choice ("random"): 0 = uniform over the other workers;
+                                      1 = die-aware: gtap_init measures the SM -> L2-die map and which die homes
+                                      each worker's deque line (gtap_ubench_die_probe), and 3 of 4 probing
+                                      lanes then draw victims whose deque line is near the thief's die */
+    uint32_t reserved2;
 } gtap_config;
 
 typedef struct gtap_runtime gtap_runtime;
@@ -311,6 +316,15 @@ const gtap_task_table *gtap_table_bfs_ex(const int32_t *row_ptr, const int32_t *
 gtap_status gtap_bfs_init_depth(int32_t *depth, uint32_t nv, int32_t src, void *stream);
 
 /* ---- microbenchmarks (roofline denominators) ----------- */
+
+/* SM -> L2-die map (SURVEY.md §8(d) probe (vi)), synchronous on `stream`: one block per SM, in turn,
+ * times dependent strong (L2) loads to n_addr addresses spaced bytes / n_addr apart in d_buf (>= 2 KB apart
+ * to see distinct L2 homes). h_sm_die[smid] (sm_cap entries) = 0 for SM 0's die, 1 for the other;
+ * h_addr_near[k] (may be NULL) = the die whose SMs reach address k faster; h_out3 (may be NULL) = {mean
+ * near latency, mean far latency (cycles), consistency = mean fraction of addresses on which an SM's
+ * near/far pattern matches its die}. Needs the GPU to itself (timing). */
+gtap_status gtap_ubench_die_probe(const void *d_buf, uint64_t bytes, uint32_t n_addr, uint8_t *h_sm_die,
+                                  uint32_t sm_cap, uint8_t *h_addr_near, float *h_out3, void *stream);
 
 /* L2-atomic throughput probe on `stream`, synchronous. kind: 0 atom.add with
  * return on distinct words (the join decrement), 1 red.add (no return),

@@ -89,7 +89,14 @@ struct __align__(128) Ctl {
     long long outstanding;    // no-taskwait termination counter (SPEC S:321 reading)
     uint32_t pad2[30];
     uint32_t roots_left;      // taskwait-closed termination: roots not yet finished
-    uint32_t pad3[31];
+    // victim_policy 1 (die-aware stealing): vinfo = device {sm_die[256 bytes], vlist[]} -- the workers whose
+    // deque line is homed in die 0's / die 1's L2 are vlist[0, vcnt[0]) / vlist[vcnt[2], vcnt[2] + vcnt[1]),
+    // counts restricted to the run's workers; vinfo nullptr = uniform victims. Staged with the control block,
+    // read-only during the run (kept out of KParams: a larger kernel-parameter block cost the fib kernel 13
+    // registers)
+    uint32_t vcnt[3];
+    uint32_t pad3[25];
+    const uint32_t* vinfo;
     unsigned long long stats[ST_COUNT];
     uint32_t pad4[32];
 };
@@ -142,7 +149,14 @@ struct KParams {
     const RootSpec* roots;   // nroots
     long long* root_results; // nroots
     CheckBuf* chk;           // GTAP_CHECK builds only (else nullptr)
+    // victim_policy 1 (die-aware stealing): die of every SM, and the workers whose deque metadata line is
+    // homed in die 0's / die 1's L2 (vlist[0, vcnt0) / vlist[vcnt0, vcnt0 + vcnt1)); nullptr: uniform victims
 };
+
+// die-aware victim choice: 3 of 4 probing lanes draw from the workers whose deque line is
+// near the thief's die (their steal CAS and lock RMW stay in the near L2), the rest uniformly
+int die_probe(const void* base, uint64_t stride, uint32_t n, uint8_t* sm_die, uint32_t cap, uint8_t* addr_near,
+              float* out3, cudaStream_t s);
 
 // Host-side layout of the workspace (offsets in bytes).
 struct Layout {
@@ -321,18 +335,41 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 }
 __device__ __forceinline__ void nanosleep(uint32_t ns) { asm volatile("nanosleep.u32 %0;" ::"r"(ns)); }
 
-__device__ __forceinline__ uint32_t lanemask_lt() {
-    uint32_t m;
-    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
-    return m;
+__device__ __forceinline__ uint32_t smid() {
+    uint32_t s;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(s));
+    return s;
 }
-
 __device__ __forceinline__ uint32_t xorshift32(uint32_t& s) {
     s ^= s << 13;
     s ^= s >> 17;
     s ^= s << 5;
     return s;
 }
+
+// a steal victim != w from the random draw r: with victim_policy 1 (vinfo != nullptr) lanes < 24 draw from the
+// workers whose deque line is near the thief's die, the others uniformly
+__device__ __forceinline__ uint32_t pick_victim(uint32_t W, uint32_t w, uint32_t lane, uint32_t r, const Ctl* ctl) {
+    if (lane < 24u) {
+        const uint32_t* vi = reinterpret_cast<const uint32_t*>(__ldg(reinterpret_cast<const unsigned long long*>(&ctl->vinfo)));
+        if (vi != nullptr) {
+            const uint32_t mydie = __ldg(reinterpret_cast<const uint8_t*>(vi) + smid());
+            const uint32_t cnt = __ldg(&ctl->vcnt[mydie]);
+            if (cnt > 1u) {
+                const uint32_t v = __ldg(vi + 64 + (mydie ? __ldg(&ctl->vcnt[2]) : 0u) + r % cnt);
+                return v != w ? v : (v + 1u < W ? v + 1u : 0u);
+            }
+        }
+    }
+    const uint32_t v = r % (W - 1u);
+    return v + (v >= w);
+}
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
 
 __device__ __forceinline__ uint32_t hash32(unsigned long long x) {
     x ^= x >> 33;

@@ -46,6 +46,9 @@ struct gtap_runtime {
     uint32_t run_nroots;
     gtap_status last_launch;
     gtap::CheckBuf* chk;   // GTAP_CHECK builds: device check buffer (header + 3 token arrays)
+    // victim_policy 1: device copy of {sm_die[256] | vlist[W_alloc]} and the host lists (ascending worker ids)
+    unsigned char* vbuf;
+    std::vector<uint32_t> vl[2];
 };
 
 namespace {
@@ -80,6 +83,7 @@ gtap_status resolve(const gtap_config* in, gtap_config* c, int sm_count) {
     if (c->idle_backoff_ns == 0) c->idle_backoff_ns = 8192;
     if (c->idle_backoff_ns < 32 || c->idle_backoff_ns > 1000000) return GTAP_E_INVAL;
     if (c->queue_policy > 1) return GTAP_E_INVAL;
+    if (c->victim_policy > 1) return GTAP_E_INVAL;
     const uint32_t wpb = (c->worker_kind == GTAP_WORKER_THREAD) ? c->block_size / 32 : 1;
     uint64_t W;
     if (c->grid_size) W = (uint64_t)c->grid_size * wpb;
@@ -273,6 +277,41 @@ gtap_status gtap_init(const gtap_config* in, void* d_workspace, size_t bytes, gt
 #ifdef GTAP_CHECK
     if (cudaMalloc(&rt->chk, check_bytes(rt)) != cudaSuccess) { gtap_finalize(rt); return GTAP_E_NOMEM; }
 #endif
+    if (c.victim_policy == 1u) {
+        // which die homes each worker's deque line (2 KB L2-home granules of the DequeMeta array), and the
+        // SM -> die map: one probe address per granule
+        const uintptr_t dq = (uintptr_t)(rt->ws + rt->L.dq);
+        const size_t bytes = sizeof(gtap::DequeMeta) * (size_t)rt->W_alloc * c.num_queues;
+        const uintptr_t g0 = dq / 2048u, g1 = (dq + bytes - 1u) / 2048u;
+        const uint32_t ng = (uint32_t)(g1 - g0 + 1u);
+        // one probe address per full granule (from the first 2 KB boundary inside the array); workers whose
+        // line lies in the partial first granule are left out of both lists (uniform lanes still reach them)
+        std::vector<uint8_t> gnear(ng, 2u), smd(256);
+        const uintptr_t first_full = (dq % 2048u) ? (g0 + 1u) * 2048u : dq;
+        const uint32_t nfull = first_full / 2048u <= g1 ? (uint32_t)(g1 - first_full / 2048u + 1u) : 0u;
+        // (an array inside one partial granule -- a handful of workers -- leaves both lists empty: uniform victims)
+        if (nfull > 0u && gtap::die_probe(reinterpret_cast<const void*>(first_full), 2048, nfull, smd.data(), 256,
+                                          gnear.data() + (first_full / 2048u - g0), nullptr, 0) != 0) {
+            gtap_finalize(rt);
+            return GTAP_E_CUDA;
+        }
+        for (uint32_t w = 0; w < rt->W_alloc; ++w) {
+            const uintptr_t a = dq + sizeof(gtap::DequeMeta) * (size_t)w * c.num_queues;
+            const uint8_t d = gnear[a / 2048u - g0];
+            if (d < 2u) rt->vl[d].push_back(w);
+        }
+        if (cudaMalloc(&rt->vbuf, 256 + sizeof(uint32_t) * (size_t)rt->W_alloc) != cudaSuccess) {
+            gtap_finalize(rt);
+            return GTAP_E_NOMEM;
+        }
+        std::vector<uint32_t> all(rt->vl[0]);
+        all.insert(all.end(), rt->vl[1].begin(), rt->vl[1].end());
+        if (cudaMemcpy(rt->vbuf, smd.data(), 256, cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(rt->vbuf + 256, all.data(), sizeof(uint32_t) * all.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+            gtap_finalize(rt);
+            return GTAP_E_CUDA;
+        }
+    }
     rt->dirty = true;
     if ((st = do_reset(rt, 0)) != GTAP_OK || cudaStreamSynchronize(0) != cudaSuccess) {
         gtap_finalize(rt);
@@ -336,6 +375,13 @@ static gtap_status run_impl(gtap_runtime* rt, cudaStream_t s) {
     std::memset(rt->h_ctl, 0, sizeof(Ctl));
     rt->h_ctl->roots_left = nroots;
     rt->h_ctl->outstanding = nroots;
+    rt->h_ctl->vinfo = nullptr;
+    if (rt->vbuf) {   // victim_policy 1: the lists restricted to this run's workers (ids < W, lists ascending)
+        rt->h_ctl->vcnt[0] = (uint32_t)(std::lower_bound(rt->vl[0].begin(), rt->vl[0].end(), W) - rt->vl[0].begin());
+        rt->h_ctl->vcnt[1] = (uint32_t)(std::lower_bound(rt->vl[1].begin(), rt->vl[1].end(), W) - rt->vl[1].begin());
+        rt->h_ctl->vcnt[2] = (uint32_t)rt->vl[0].size();
+        rt->h_ctl->vinfo = reinterpret_cast<const uint32_t*>(rt->vbuf);
+    }
     // one SM kernel reads both from the mapped host buffers (no copy engine, see word_copy_kernel)
     static_assert(sizeof(RootSpec) % 4 == 0 && sizeof(Ctl) % 4 == 0, "word copies");
     word_copy_kernel<<<1, 256, 0, s>>>(reinterpret_cast<const uint32_t*>(rt->dh_roots),
@@ -485,6 +531,7 @@ gtap_status gtap_finalize(gtap_runtime* rt) {
     if (rt->in_flight) cudaEventSynchronize(rt->ev2);
     if (rt->owns_ws && rt->ws) cudaFree(rt->ws);
     if (rt->chk) cudaFree(rt->chk);
+    if (rt->vbuf) cudaFree(rt->vbuf);
     if (rt->h_roots) cudaFreeHost(rt->h_roots);
     if (rt->h_ctl) cudaFreeHost(rt->h_ctl);
     if (rt->ev0) cudaEventDestroy(rt->ev0);

@@ -337,8 +337,7 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
             // a long-idle warp probes once per wake-up (keeps idle L2 traffic off busy workers)
             const uint32_t rounds = backoff >= 4096u ? 1u : p.steal_rounds;
             for (uint32_t round = 0; round < rounds && n == 0; ++round) {
-                uint32_t v = xorshift32(rng) % (p.W - 1u);
-                v += (v >= w);
+                const uint32_t v = pick_victim(p.W, w, lane, xorshift32(rng), p.ctl);
                 const uint32_t vq = (qc + lane) % (uint32_t)NQ;  // EPAQ: round-robin from the own position
                 const uint32_t vd = v * p.nq + vq;
                 const unsigned long long sv = ld_relaxed(&p.dq[vd].S);

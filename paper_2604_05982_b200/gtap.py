@@ -41,6 +41,7 @@ class Config(ctypes.Structure):
         ("steal_attempts", ctypes.c_uint32), ("steal_max", ctypes.c_uint32), ("max_roots", ctypes.c_uint32),
         ("seed", ctypes.c_uint64), ("watchdog_ns", ctypes.c_uint64),
         ("idle_backoff_ns", ctypes.c_uint32), ("queue_policy", ctypes.c_uint32),
+        ("victim_policy", ctypes.c_uint32), ("reserved2", ctypes.c_uint32),
     ]
 
 
@@ -64,7 +65,7 @@ EXPORTS = [
     "gtap_spawn_root", "gtap_reset", "gtap_run", "gtap_sync", "gtap_root_result", "gtap_finalize",
     "gtap_geometry", "gtap_table_destroy", "gtap_table_fib", "gtap_table_fib_cutoff", "gtap_table_nqueens", "gtap_table_nqueens_ex", "gtap_table_tree", "gtap_table_mergesort", "gtap_table_mergesort_ex", "gtap_table_cilksort", "gtap_table_cilksort_ex",
     "gtap_table_spmv",
-    "gtap_table_bfs", "gtap_table_bfs_ex", "gtap_bfs_init_depth", "gtap_ubench_atomics", "gtap_check_read",
+    "gtap_table_bfs", "gtap_table_bfs_ex", "gtap_bfs_init_depth", "gtap_ubench_atomics", "gtap_ubench_die_probe", "gtap_check_read",
 ]
 
 _lib = None
@@ -124,9 +125,10 @@ def lib():
     L.gtap_bfs_init_depth.argtypes = [vp, u32, i32, vp]
     L.gtap_ubench_atomics.argtypes = [vp, u64, u32, u32, u32, u32, vp, P(ctypes.c_float)]
     L.gtap_check_read.argtypes = [vp, P(u64), u32]
+    L.gtap_ubench_die_probe.argtypes = [vp, u64, u32, vp, u32, vp, vp, vp]
     for name in ("gtap_config_default", "gtap_init", "gtap_spawn_root", "gtap_reset", "gtap_run", "gtap_sync",
                  "gtap_root_result", "gtap_finalize", "gtap_geometry", "gtap_ubench_atomics", "gtap_bfs_init_depth",
-                 "gtap_check_read"):
+                 "gtap_check_read", "gtap_ubench_die_probe"):
         getattr(L, name).restype = ctypes.c_int
     _lib = L
     return L
@@ -271,6 +273,7 @@ class Runtime:
                  max_tasks_per_worker: int = 0, queue_capacity: int = 0, steal_attempts: int = 0,
                  steal_max: int = 0, seed: int = 0x5EED, watchdog_ns: int = 0, max_roots: int = 0,
                  idle_backoff_ns: int = 0, num_queues: int = 0, max_child_tasks: int = 0, queue_policy: int = 0,
+                 victim_policy: int = 0,
                  torch_workspace: bool = True):
         import torch
         L = lib()
@@ -279,7 +282,8 @@ class Runtime:
         for k, v in dict(grid_size=grid_size, block_size=block_size, max_tasks_per_worker=max_tasks_per_worker,
                          queue_capacity=queue_capacity, steal_attempts=steal_attempts, steal_max=steal_max,
                          watchdog_ns=watchdog_ns, max_roots=max_roots, idle_backoff_ns=idle_backoff_ns,
-                         num_queues=num_queues, max_child_tasks=max_child_tasks, queue_policy=queue_policy).items():
+                         num_queues=num_queues, max_child_tasks=max_child_tasks, queue_policy=queue_policy,
+                         victim_policy=victim_policy).items():
             if v:
                 setattr(cfg, k, v)
         cfg.seed = seed
@@ -366,6 +370,19 @@ def ubench_atomics(buf, kind: int, grid: int, block: int, ops_per_thread: int, s
     _check(lib().gtap_ubench_atomics(buf.data_ptr(), buf.numel(), kind, grid, block, ops_per_thread,
                                      _stream_ptr(stream), ctypes.byref(ms)), "gtap_ubench_atomics")
     return ms.value
+
+
+def ubench_die_probe(buf, n_addr: int = 256, stream=None) -> dict:
+    """SM -> L2-die map measured over n_addr addresses of the CUDA tensor buf (gtap.h gtap_ubench_die_probe)."""
+    import numpy as np
+    sm_die = np.zeros(256, np.uint8)
+    near = np.zeros(n_addr, np.uint8)
+    out3 = np.zeros(3, np.float32)
+    _check(lib().gtap_ubench_die_probe(buf.data_ptr(), buf.numel() * buf.element_size(), n_addr,
+                                       sm_die.ctypes.data, 256, near.ctypes.data, out3.ctypes.data,
+                                       _stream_ptr(stream)), "gtap_ubench_die_probe")
+    return dict(sm_die=sm_die, addr_near=near, near_cycles=float(out3[0]), far_cycles=float(out3[1]),
+                consistency=float(out3[2]))
 
 
 def bfs_init_depth(depth, src: int, stream=None):

@@ -140,3 +140,13 @@ def test_fifo_order_overflow_fails_loudly(g):
         with pytest.raises(g.GtapError) as e:
             check(g, r, rp, col, src, order=1)
         assert e.value.code in (5, 6)
+
+
+def test_die_aware_victims_block_level(g):
+    """victim_policy 1 on block-level workers (BFS): same levels."""
+    rp, col = synth.rmat_csr(14, 16, seed=14)
+    with g.Runtime(g.GTAP_WORKER_BLOCK, 0, grid_size=148 * 4, block_size=64, max_tasks_per_worker=1 << 15,
+                   steal_max=32, victim_policy=1, watchdog_ns=WD) as r:
+        for s in synth.bfs_sources(rp, 2, seed=14):
+            check(g, r, rp, col, s)
+            check(g, r, rp, col, s, order=1)

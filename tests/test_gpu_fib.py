@@ -116,3 +116,14 @@ def test_bad_root_rejected(g, rt):
     with pytest.raises(g.GtapError):
         rt.spawn_root(t, (47,))  # int32 overflow (reading R17)
     t.close()
+
+
+@pytest.mark.parametrize("grid,block", [(148, 128), (0, 128), (3, 64)])
+def test_fib_die_aware_victims(g, grid, block):
+    """victim_policy 1 (gtap_init probes the SM -> L2-die map; thieves favour victims whose deque line is near
+    their die): a scheduling choice only -- values and counts stay exact."""
+    with g.Runtime(g.GTAP_WORKER_THREAD, 0, grid_size=grid, block_size=block, max_tasks_per_worker=4096,
+                   victim_policy=1, watchdog_ns=WD) as r:
+        for n in (5, 20, 27):
+            v, st = g.fib(n, rt=r)
+            assert (v, st.tasks, st.invocations) == oracle.fib(n)

@@ -102,3 +102,19 @@ def test_max_child_tasks_enforced(g):
         with pytest.raises(g.GtapError) as e:
             g.spmv(rp.to(dev), col.to(dev), val.to(dev), x.to(dev), nnz_cut=256, fanout=4, rt=r)
         assert e.value.code == 7
+
+
+def test_die_probe_map(cuda_device):
+    """gtap_ubench_die_probe: every SM gets a die label, both dies are populated, far latency > near."""
+    import torch
+
+    import paper_2604_05982_b200 as g
+    from paper_2604_05982_b200 import gtap
+    buf = torch.zeros(128 * 2048 // 4, dtype=torch.int32, device="cuda")
+    r = gtap.ubench_die_probe(buf, 128)
+    nsm = torch.cuda.get_device_properties(0).multi_processor_count
+    die = r["sm_die"][:nsm]
+    assert set(die.tolist()) <= {0, 1} and 0 < int(die.sum()) < nsm
+    assert r["far_cycles"] > r["near_cycles"] > 0
+    with pytest.raises(g.GtapError):
+        g.Runtime(g.GTAP_WORKER_THREAD, 0, victim_policy=2)

@@ -809,7 +809,7 @@ struct GBoard {
 // merges up to this many keys run as one bitonic network when the bulk-copy core is available (larger ones:
 // the core); without it, up to kBitonicMax
 #ifndef GTAP_MS_BITONIC_MAX
-#define GTAP_MS_BITONIC_MAX 256
+#define GTAP_MS_BITONIC_MAX 512
 #endif
 constexpr uint32_t kMsBitonicMax = GTAP_MS_BITONIC_MAX;
 

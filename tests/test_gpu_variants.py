@@ -7,7 +7,7 @@ oracle: the options are alternative implementations of the same task bodies / sc
 
 * GTAP_FSTACK=1, GTAP_FIB_FSTACK=1: a one-entry own free stack, so nearly every surplus free takes
   the overflow path to the home free ring (fib, trees, Cilksort, N-Queens).
-* GTAP_MS_VT=23, GTAP_MS_BITONIC_MAX=1024: the bulk-copy merge core with 736-key tiles (default 480) and bitonic merges up to 1024 keys (default 256).
+* GTAP_MS_VT=23, GTAP_MS_BITONIC_MAX=1024: the bulk-copy merge core with 736-key tiles (default 480) and bitonic merges up to 1024 keys (default 512).
 * GTAP_CS_KARY=0: Cilksort's plain binary split search.
 * GTAP_BFS_POP_BATCH=0 / 32: single pops and the largest batch pop of the block-level leader;
   GTAP_BFS_SKIP_STALE=1: a task whose vertex improved since its spawn returns at once (measured slower).

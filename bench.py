@@ -63,9 +63,9 @@ FIB_FOREST_ROOTS = 64    # strong scaling: 64 roots of fib(32) dealt over the ra
 FIB_FOREST_N = 32
 SPMV_ROWS = 1 << 22
 SPMV_NNZ_CUT = 65536
-SPMV_FANOUT = 32
-SPMV_PARTS = 148 * 8     # forest: one nnz-balanced root per worker (fn part(k, R), reading R20)
-SPMV_CFG = dict(grid_size=148 * 8, block_size=128, max_tasks_per_worker=1024, max_roots=SPMV_PARTS)
+SPMV_FANOUT = 4          # a root range above the cut splits into 4 (fanout 32 made ~3 K-nnz slivers)
+SPMV_PARTS = 148 * 4     # forest: one nnz-balanced root per worker (fn part(k, R), reading R20)
+SPMV_CFG = dict(grid_size=148 * 4, block_size=256, max_tasks_per_worker=1024, max_roots=SPMV_PARTS)
 CS_CFG = dict(grid_size=0, block_size=128, max_tasks_per_worker=4096, idle_backoff_ns=1024)
 NQ_N = 16
 NQ_CUTOFF = 7

@@ -10,7 +10,8 @@ oracle: the options are alternative implementations of the same task bodies / sc
 * GTAP_MS_VT=23, GTAP_MS_BITONIC_MAX=1024: the bulk-copy merge core with 736-key tiles (default 480) and bitonic merges up to 1024 keys (default 512).
 * GTAP_CS_KARY=0: Cilksort's plain binary split search.
 * GTAP_BFS_POP_BATCH=0 / 32: single pops and the largest batch pop of the block-level leader;
-  GTAP_BFS_SKIP_STALE=1: a task whose vertex improved since its spawn returns at once (measured slower).
+  GTAP_BFS_SKIP_STALE=1: a task whose vertex improved since its spawn returns at once (measured slower);
+  GTAP_BFS_TTAS=0: every scanned edge issues its atomicMin (the default reads depth[u] first).
 """
 import json
 import os
@@ -95,8 +96,9 @@ def _probe(lib, what):
     (("GTAP_BFS_POP_BATCH=0",), "bfs"),
     (("GTAP_BFS_POP_BATCH=32",), "bfs"),
     (("GTAP_BFS_SKIP_STALE=1",), "bfs"),
+    (("GTAP_BFS_TTAS=0",), "bfs"),
 ], ids=["fstack1", "ms_vt23_bitonic1024", "cs_binary_split", "bfs_pop1",
-        "bfs_pop32", "bfs_skip_stale"])
+        "bfs_pop32", "bfs_skip_stale", "bfs_atomic_always"])
 def test_variant_parity(cuda_device, defines, what):
     lib = _variant(defines)
     res = _probe(lib, what)

@@ -50,6 +50,14 @@ for k in sorted(set(kind.tolist())):
         print(f"{KIND[k]:12s} size={size:9d} n={sel.sum():6d} start={(t0[sel].min() - base) / 1e6:7.3f} "
               f"end={(t1[sel].max() - base) / 1e6:7.3f} ms  dur_us mean={d.mean():8.1f} max={d.max():8.1f}")
 
+# scheduler share: warp time outside task bodies = 1 - (leaf sorts + warp-assisted merges + GPU-wide chunks, kinds
+# 2, 3, 6, 7) / (workers x span); requester records 4 / 5 overlap their own chunk records and are excluded
+body = float(((t1 - t0)[np.isin(kind, [2, 3, 6, 7])]).sum())
+W = st.workers
+span = float(t1.max() - base)
+print(f"workers {W}: task-body share of warp time {body / (W * span):.3f}, scheduler + idle {1 - body / (W * span):.3f} "
+      f"(span {span / 1e6:.3f} ms)")
+
 # timeline: average number of warps busy per 50 us bin, by record class (requester records 4/5 excluded:
 # their warps' chunk work is recorded as kinds 6/7)
 BIN = 50_000

@@ -59,6 +59,9 @@ MS_MERGE_MODE = 1        # GTAP_MERGE_WARP: leaf/merge bodies run by the task's 
 MS0_CFG = dict(grid_size=0, block_size=128, max_tasks_per_worker=1024, idle_backoff_ns=32768)  # one-lane merge
 FIB_N = 40
 FIB_CFG = dict(grid_size=0, block_size=128, max_tasks_per_worker=4096)
+# fib(20) is launch + span bound: a smaller persistent grid starts and drains faster (grid 0 = 1,184 x 128:
+# 150 us; 148 x 64 with a 256 ns idle-backoff cap: 105 us; fib(0) alone: 46 vs 12 us), P:943-948 GRID_SIZE
+FIB20_CFG = dict(grid_size=148, block_size=64, max_tasks_per_worker=4096, idle_backoff_ns=256)
 FIB_FOREST_ROOTS = 64    # strong scaling: 64 roots of fib(32) dealt over the ranks
 FIB_FOREST_N = 32
 SPMV_ROWS = 1 << 22
@@ -431,9 +434,7 @@ def bench_fib20(dev, ws=1, reps=20):
     """BASELINE configs[0] / SURVEY §8(d) C1: fib(20) (21,891 tasks) is span-bound -- its critical path is
     2n - 1 = 39 dependent invocations -- so it is reported as tasks/s and as time per critical-path step."""
     import paper_2604_05982_b200 as g
-    # a short idle backoff: at fib(20) idle warps polling for the few runnable tasks are on the critical
-    # path (8192 ns cap: 0.198 ms, 1024 ns: 0.145 ms; fib(40) prefers 8192, bench_tools/fib_backoff.py)
-    rt = g.Runtime(g.GTAP_WORKER_THREAD, dev.index, **dict(FIB_CFG, idle_backoff_ns=1024))
+    rt = g.Runtime(g.GTAP_WORKER_THREAD, dev.index, **FIB20_CFG)
     ms = []
     st = None
     for i in range(reps + 1):

@@ -1,6 +1,6 @@
 """Small runs of the hot tables for compute-sanitizer (memcheck / racecheck / synccheck / initcheck).
 
-usage: compute-sanitizer --tool <tool> python bench_tools/sanitize_probe.py <fib|ms|ms0|spmv|bfs|tree|cs|nq>
+usage: compute-sanitizer --tool <tool> python bench_tools/sanitize_probe.py <fib|ms|ms0|spmv|bfs|bfs1|tree|cs|nq|fibdie>
 
 Each run is checked against the oracle so a sanitizer-clean run is also a correct one; sizes are small
 (the sanitizers slow every memory access down by 10-100x) but span several workers, steals and, for
@@ -20,8 +20,9 @@ import paper_2604_05982_b200 as g  # noqa: E402
 
 WD = 120_000_000_000
 what = sys.argv[1]
-if what == "fib":
-    v, st = g.fib(16, grid_size=148, block_size=128, max_tasks_per_worker=1024, watchdog_ns=WD)
+if what in ("fib", "fibdie"):
+    v, st = g.fib(16, grid_size=148, block_size=128, max_tasks_per_worker=1024, watchdog_ns=WD,
+                  victim_policy=1 if what == "fibdie" else 0)
     assert (v, st.tasks, st.invocations) == oracle.fib(16)
 elif what in ("ms", "ms0"):
     n = 1 << 17 if what == "ms" else 1 << 13
@@ -47,11 +48,11 @@ elif what == "spmv":
     y64, _ = oracle.spmv(rp, col, val, x)
     e = np.abs(y.cpu().numpy().astype(np.float64) - y64) / np.maximum(np.abs(y64), 1e-30)
     assert np.all((y64 == 0) | (e <= 1e-5))
-elif what == "bfs":
+elif what in ("bfs", "bfs1"):
     rp, col = synth.rmat_csr(10, 16, seed=4)
     src = synth.bfs_sources(rp, 1, seed=4)[0]
     depth, st = g.bfs(rp.cuda(), col.cuda(), src, grid_size=148, block_size=64, max_tasks_per_worker=1 << 14,
-                      steal_max=32, watchdog_ns=WD)
+                      steal_max=32, watchdog_ns=WD, order=1 if what == "bfs1" else 0)
     assert np.array_equal(depth.cpu().numpy(), oracle.bfs(rp, col, src))
 elif what == "tree":
     buf_cpu = synth.tree_buffer(1 << 12)

@@ -420,6 +420,7 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) block_sched_ker
                 }
             }
             if (id != kNone) {
+                __syncwarp();   // every lane read kept_fresh / the batch slots above before lane 0 rewrites them
                 if (lane == 0) {
                     L.S_pref = ld_relaxed(&mydq->S);  // consumed at finalize (publication check)
                     if (from_spec) {  // a child this block just spawned: its record is not re-read

@@ -323,6 +323,11 @@ __device__ __forceinline__ uint32_t atom_exch_relaxed(uint32_t* p, uint32_t v) {
     asm volatile("atom.relaxed.gpu.global.exch.b32 %0, [%1], %2;" : "=r"(o) : "l"(p), "r"(v) : "memory");
     return o;
 }
+__device__ __forceinline__ uint32_t atom_exch_release(uint32_t* p, uint32_t v) {
+    uint32_t o;
+    asm volatile("atom.release.gpu.global.exch.b32 %0, [%1], %2;" : "=r"(o) : "l"(p), "r"(v) : "memory");
+    return o;
+}
 __device__ __forceinline__ void red_add_relaxed(uint32_t* p, uint32_t v) {
     asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }

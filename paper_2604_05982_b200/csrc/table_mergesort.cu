@@ -1024,9 +1024,9 @@ struct MergesortTable {
         if (lane == 0) {
             st_relaxed(&S->l, l); st_relaxed(&S->m, m); st_relaxed(&S->r, r); st_relaxed(&S->depth, depth);
             st_relaxed(&S->nchunks, nch); st_relaxed(&S->done, 0u);
-            __threadfence();
-            atom_exch_relaxed(&S->next, 0u);
-            __threadfence();
+            // the release RMW publishes the parameters to every claim (an acquire RMW on next) that follows it;
+            // the release store orders the reset before the slot shows as open
+            atom_exch_release(&S->next, 0u);
             st_release(&S->state, 2u);
             atomicOr(&gb->bits[sidx >> 5], 1u << (sidx & 31u));
             red_add_relaxed(&gb->open, 1u);
@@ -1044,8 +1044,7 @@ struct MergesortTable {
         if (lane == 0) {
             atom_exch_relaxed(&S->next, 0x80000000u);
             red_add_relaxed(&gb->open, 0xFFFFFFFFu);
-            __threadfence();
-            st_release(&S->state, 0u);
+            st_release(&S->state, 0u);   // orders the close (late claims fail) before the slot shows as free
         }
         __syncwarp();
         __threadfence();

@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define GTAP_ABI_VERSION 1u
+#define GTAP_ABI_VERSION 2u  /* 2: gtap_config gained queue_policy / victim_policy (round 2) */
 
 typedef enum {
     GTAP_OK = 0,

@@ -59,6 +59,8 @@ class Stats(ctypes.Structure):
         return {k: (getattr(self, k) if k != "reserved" else None) for k, _ in self._fields_ if k != "reserved"}
 
 
+ABI_VERSION = 2  # include/gtap.h GTAP_ABI_VERSION
+
 # Every symbol include/gtap.h declares (checked by tests/test_abi.py).
 EXPORTS = [
     "gtap_abi_version", "gtap_status_str", "gtap_config_default", "gtap_workspace_bytes", "gtap_init",
@@ -130,6 +132,8 @@ def lib():
                  "gtap_root_result", "gtap_finalize", "gtap_geometry", "gtap_ubench_atomics", "gtap_bfs_init_depth",
                  "gtap_check_read", "gtap_ubench_die_probe"):
         getattr(L, name).restype = ctypes.c_int
+    if L.gtap_abi_version() != ABI_VERSION:
+        raise ImportError(f"{LIB_PATH}: ABI version {L.gtap_abi_version()} != binding's {ABI_VERSION}; rebuild")
     _lib = L
     return L
 

@@ -52,7 +52,8 @@ def test_sm100a_cubin(libgtap):
 
 
 def test_status_strings_and_version(libgtap):
-    assert libgtap.gtap_abi_version() == 1
+    from paper_2604_05982_b200 import gtap
+    assert libgtap.gtap_abi_version() == 2 == gtap.ABI_VERSION
     assert libgtap.gtap_status_str(5) == b"GTAP_E_POOL_EXHAUSTED"
     assert libgtap.gtap_status_str(0) == b"GTAP_OK"
 

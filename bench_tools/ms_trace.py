@@ -99,3 +99,40 @@ if top is not None and top.any():
     print(f"  chunk dur p10 {np.percentile(d, 10):.1f} p50 {np.percentile(d, 50):.1f} p90 {np.percentile(d, 90):.1f} max {d.max():.1f} us")
     last = np.array([t1[ch][ws == w].max() for w in uw])
     print(f"  last chunk end before close: p10 {(te - np.percentile(last, 90)) / 1e3:.1f} p50 {(te - np.percentile(last, 50)) / 1e3:.1f} us")
+
+# GPU-wide phase: per 20 us bin, warps merging chunks (busy) vs chunks open but unclaimed (demand); a bin with
+# idle warps AND unclaimed chunks loses time to discovery, one with idle warps and no demand to the DAG
+# (parents waiting for their last chunks / join-to-open latency)
+req = np.where(kind == 5)[0]
+if len(req):
+    spl = np.where(kind == 8)[0]
+    spos, st0 = (buf[spl, 2] & np.uint64(0xFFFFFFFF)).astype(np.int64), t0[spl]
+    rpos = (buf[req, 2] & np.uint64(0xFFFFFFFF)).astype(np.int64)
+    claims = []   # per slot: sorted claim times
+    for i, j in enumerate(req):
+        sel = (spos >= rpos[i]) & (spos < rpos[i] + sz[j]) & (st0 >= t0[j]) & (st0 <= t1[j])
+        claims.append(np.sort(st0[sel]))
+    BIN2 = 20_000
+    g0 = t0[req].min()
+    print("GPU phase (20 us bins): t_us  busy_chunk_warps  unclaimed_chunks  open_slots")
+    for t in range(int(g0), int(t1.max()), BIN2):
+        tm = t + BIN2 // 2
+        openm = (t0[req] <= tm) & (t1[req] > tm)
+        un = 0
+        for i in np.where(openm)[0]:
+            nch = (sz[req[i]] + 4095) // 4096
+            un += nch - int(np.searchsorted(claims[i], tm))
+        ch = (kind == 6)
+        busy = ((t0[ch] <= tm) & (t1[ch] > tm)).sum() + ((kind == 8) & (t0 <= tm) & (t1 > tm)).sum()
+        print(f"  {(t - base) / 1e3:8.0f} {busy:6d} {un:7d} {openm.sum():5d}")
+    # join-to-open: a parent slot opens after the later of its two children's slots closed
+    ends = {(int(rpos[i]), int(sz[j])): t1[j] for i, j in enumerate(req)}
+    lat = {}
+    for i, j in enumerate(req):
+        s, p = int(sz[j]), int(rpos[i])
+        c1, c2 = ends.get((p, s // 2)), ends.get((p + s // 2, s - s // 2))
+        if c1 is not None and c2 is not None:
+            lat.setdefault(s, []).append((t0[j] - max(c1, c2)) / 1e3)
+    for s in sorted(lat):
+        v = np.array(lat[s])
+        print(f"  join->open size {s:9d}: n {len(v):4d} p50 {np.percentile(v, 50):6.2f} p90 {np.percentile(v, 90):6.2f} us")

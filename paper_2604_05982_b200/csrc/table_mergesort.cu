@@ -785,6 +785,12 @@ constexpr uint32_t kGSlots = 1024;
 #ifndef GTAP_MS_GCHUNK
 #define GTAP_MS_GCHUNK 4096   // 2048 / 3072 / 4096 / 6144: 1.51 / 1.46 / 1.44 / 1.50 ms at 2^24
 #endif
+#ifndef GTAP_MS_KEEP_GLOBAL
+#define GTAP_MS_KEEP_GLOBAL 1   // 0: 1.40 ms, 1: 1.38 ms at 2^24
+#endif
+#ifndef GTAP_MS_REQ_HELP
+#define GTAP_MS_REQ_HELP 0      // 1: a requester whose chunks are all claimed helps other open slots (1.38 vs 1.32 ms: it closes late)
+#endif
 constexpr uint32_t kGlobalAssistMin = GTAP_MS_GLOBAL_MIN;
 constexpr uint32_t kGChunk = GTAP_MS_GCHUNK;
 // chunk c of an n-key merge: output range [c * kGChunk, min(n, (c + 1) * kGChunk)) (uniform chunks; a
@@ -840,6 +846,12 @@ struct MergesortTable {
     static constexpr bool kHasHeavy = true;
     __device__ __forceinline__ static bool heavy(uint32_t, const uint32_t* d) { return d[1] - d[0] >= kTmaMin; }
     __device__ __forceinline__ static bool heavy_parent(uint32_t, const uint32_t* d) {
+#if GTAP_MS_KEEP_GLOBAL
+        // a resumed parent whose merge goes to the GPU-wide board stays in the kept set: every idle warp
+        // helps that merge anyway, and a push + publish + reclaim would add round trips to the top levels'
+        // critical path (join -> slot open)
+        if (MODE == 1u && 2u * (d[1] - d[0]) >= kGlobalAssistMin) return false;
+#endif
         return 2u * (d[1] - d[0]) >= kTmaMin;
     }
     static constexpr int kMaxThreads = 128;                    // __launch_bounds__
@@ -1034,11 +1046,11 @@ struct MergesortTable {
         }
         __syncwarp();
         gchunks(a, S, lane, H);
-        while (true) {   // wait for the helpers; meanwhile help other open slots
+        while (true) {   // wait for the helpers (GTAP_MS_REQ_HELP: meanwhile help other open slots)
             uint32_t dn = 0;
             if (lane == 0) dn = ld_relaxed(&S->done);
             if (__shfl_sync(0xffffffffu, dn, 0) >= nch) break;
-            if (!help_global_once(a, lane, H) && lane == 0) nanosleep(256);
+            if (!(GTAP_MS_REQ_HELP && help_global_once(a, lane, H)) && lane == 0) nanosleep(256);
             __syncwarp();
         }
         if (lane == 0) {

@@ -795,9 +795,32 @@ constexpr uint32_t kGlobalAssistMin = GTAP_MS_GLOBAL_MIN;
 constexpr uint32_t kGChunk = GTAP_MS_GCHUNK;
 // chunk c of an n-key merge: output range [c * kGChunk, min(n, (c + 1) * kGChunk)) (uniform chunks; a
 // tail of shorter chunks measured slower: 1024 / 2048-key tails 1.51 / 1.47 ms vs 1.45 at 2^24)
-__device__ __forceinline__ uint32_t gch_count(uint32_t n) { return (n + kGChunk - 1u) / kGChunk; }
-__device__ __forceinline__ uint2 gch_range(uint32_t n, uint32_t c) {
-    return make_uint2(c * kGChunk, min(n, c * kGChunk + kGChunk));
+#ifndef GTAP_MS_GCH_TOP
+#define GTAP_MS_GCH_TOP 2   // 0 / 2 / 4 / 8: 1.312 / 1.306 / 1.310 / 1.319 ms at 2^24; merges of >= n_array / GTAP_MS_GCH_TOP keys: one chunk per warp share (0: off)
+#endif
+__device__ __forceinline__ uint32_t gch_count(uint32_t n, uint32_t n_all) {
+    uint32_t c = (n + kGChunk - 1u) / kGChunk;
+#if GTAP_MS_GCH_TOP
+    // the top levels' merges run (nearly) alone on the GPU: a merge of n of the array's n_all keys is cut into its
+    // share n W / n_all of the grid's W warps (one chunk per warp, 2^24 keys: 2368 chunks of ~7085 keys), so the
+    // fixed cost of a chunk (split search, ring fill, store drain: ~10 us) is paid once per warp and level
+    // instead of in 1.73 rounds of 4096-key chunks
+    const uint32_t W = gridDim.x * (blockDim.x >> 5);
+    if ((unsigned long long)n * GTAP_MS_GCH_TOP >= n_all) {
+        const uint32_t cw = (uint32_t)(((unsigned long long)n * W + n_all - 1u) / n_all);
+        c = max(1u, min(c, cw));
+    }
+#endif
+    (void)n_all;
+    return c;
+}
+// chunk c of the nch chunks of an n-key merge: the kGChunk grid when nch = ceil(n / kGChunk), else the output
+// range [c n / nch, (c + 1) n / nch), inner bounds rounded down to a multiple of 4 (16-B aligned bulk stores)
+__device__ __forceinline__ uint2 gch_range(uint32_t n, uint32_t c, uint32_t nch) {
+    if (nch == (n + kGChunk - 1u) / kGChunk) return make_uint2(c * kGChunk, min(n, c * kGChunk + kGChunk));
+    const uint32_t o0 = c == 0u ? 0u : (uint32_t)(((unsigned long long)c * n / nch) & ~3ull);
+    const uint32_t o1 = c + 1u >= nch ? n : (uint32_t)(((unsigned long long)(c + 1u) * n / nch) & ~3ull);
+    return make_uint2(o0, o1);
 }
 struct __align__(128) GSlot {
     uint32_t state, next, done, nchunks;
@@ -974,7 +997,7 @@ struct MergesortTable {
             const uint32_t l = __shfl_sync(0xffffffffu, prm.x, 0), m = __shfl_sync(0xffffffffu, prm.y, 0),
                            r = __shfl_sync(0xffffffffu, prm.z, 0), depth = __shfl_sync(0xffffffffu, prm.w, 0);
             const int32_t* src = buf(a, depth + 1u);
-            const uint2 orng = gch_range(r - l, c);
+            const uint2 orng = gch_range(r - l, c, nch);
             const uint32_t o0 = orng.x, o1 = orng.y;
             MS_T0;
             const uint2 sp = warp_split2(src, l, m, r, o0, o1, lane);
@@ -1032,7 +1055,7 @@ struct MergesortTable {
         }
         if (sidx == kNone) return false;
         GSlot* S = gb->slot + sidx;
-        const uint32_t nch = gch_count(r - l);
+        const uint32_t nch = gch_count(r - l, a.n);
         if (lane == 0) {
             st_relaxed(&S->l, l); st_relaxed(&S->m, m); st_relaxed(&S->r, r); st_relaxed(&S->depth, depth);
             st_relaxed(&S->nchunks, nch); st_relaxed(&S->done, 0u);

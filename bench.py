@@ -75,9 +75,13 @@ NQ_CUTOFF = 7
 NQ_CFG = dict(grid_size=0, block_size=128, max_tasks_per_worker=4096)
 BFS_SCALE = 22
 BFS_SOURCES = 16         # 16 seeded sources, median
-BFS_CFG = dict(grid_size=148 * 16, block_size=64, max_tasks_per_worker=1 << 18, idle_backoff_ns=1024,
-               steal_max=32)  # batch steals (the paper's block-level steal takes 1): 33 -> 8.6 ms
+# one-warp blocks, 32 per SM (the 128-entry staging kernel: 3.3 KB of shared memory per block): 2368 x 64 -> 4736 x 32
+# with hub splitting 7.8 -> 4.8 ms per source (bench_tools/bfs_ab.sh); batch steals (the paper's block-level steal
+# takes 1): 33 -> 8.6 ms at 2368 x 64
+BFS_CFG = dict(grid_size=148 * 32, block_size=32, max_tasks_per_worker=1 << 17, idle_backoff_ns=4096,
+               steal_max=32)
 BFS_ORDER = 1            # oldest-first owner pops (gtap_table_bfs_ex): 9.4 -> 8.4 ms per source
+BFS_SPLIT = 1024         # hub edge lists cut into bfs_edges pieces of this many edges (gtap_table_bfs_split; 0 = off)
 FOREST_EACH = 1 << 20    # C5b array size
 FOREST_WEAK_PER_GPU = 16
 FOREST_STRONG_TOTAL = 128
@@ -701,11 +705,11 @@ def bench_bfs(dev, ws=1, rank=0, atom_min_peak=None, nsrc_total=BFS_SOURCES):
     allsrc = synth.bfs_sources(rp, nsrc_total, seed=5)
     mine = shard.split_round_robin(nsrc_total, ws, rank)
     rt.reset()
-    g.bfs(rp, col, allsrc[0], depth, rt=rt, order=BFS_ORDER)  # warm-up (untimed)
+    g.bfs(rp, col, allsrc[0], depth, rt=rt, order=BFS_ORDER, edge_split=BFS_SPLIT)  # warm-up (untimed)
     per = []
     for k in mine:
         rt.reset()
-        depth, st = g.bfs(rp, col, allsrc[k], depth, rt=rt, order=BFS_ORDER)
+        depth, st = g.bfs(rp, col, allsrc[k], depth, rt=rt, order=BFS_ORDER, edge_split=BFS_SPLIT)
         reached = depth != 0x7FFFFFFF
         edges = int(deg[reached].sum().item()) // 2  # undirected input edges in the component (Graph500)
         per.append([float(k), edges / (st.device_ms * 1e-3), st.device_ms, float(st.tasks),
@@ -716,6 +720,7 @@ def bench_bfs(dev, ws=1, rank=0, atom_min_peak=None, nsrc_total=BFS_SOURCES):
     teps = statistics.median(p[1] for p in allper)
     out = dict(workload="BFS RMAT scale 22 ef 16 (configs[4]), block-level", metric="GTEPS", value=teps / 1e9,
                order="oldest-first owner pops (gtap_table_bfs_ex order 1)" if BFS_ORDER else "LIFO owner pops",
+               edge_split=BFS_SPLIT, grid=BFS_CFG["grid_size"], block=BFS_CFG["block_size"],
                ms=statistics.median(p[2] for p in allper), sources=len(allper),
                tasks_over_reached=statistics.median(p[3] / p[4] for p in allper),
                reached=int(statistics.median(p[4] for p in allper)))

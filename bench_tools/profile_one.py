@@ -45,6 +45,6 @@ elif wl == "bfs":
     src = synth.bfs_sources(rp, 1, seed=5)[0]
     with g.Runtime(g.GTAP_WORKER_BLOCK, 0, **bench.BFS_CFG) as rt:
         for i in range(reps):
-            d, st = g.bfs(rp, col, src, rt=rt, order=bench.BFS_ORDER)
+            d, st = g.bfs(rp, col, src, rt=rt, order=bench.BFS_ORDER, edge_split=bench.BFS_SPLIT)
             print("bfs", scale, st.device_ms, st.tasks, flush=True)
 torch.cuda.synchronize()

@@ -311,6 +311,15 @@ const gtap_task_table *gtap_table_bfs(const int32_t *row_ptr, const int32_t *col
 const gtap_task_table *gtap_table_bfs_ex(const int32_t *row_ptr, const int32_t *col,
                                          int32_t *depth, uint32_t nv, uint32_t order);
 
+/* BFS with hub splitting (a B200 decomposition, R29; the levels are the same): as
+ * gtap_table_bfs_ex, and a bfs(v) task whose vertex has more than edge_split edges spawns fn 1
+ * bfs_edges(v, lo, hi) tasks for the pieces [s + k*edge_split, ...) of its edge list beyond the first,
+ * which it scans itself; a piece re-reads depth[v] (it can only have decreased). edge_split 0 = never
+ * (= gtap_table_bfs_ex). Roots are fn 0. NULL on bad arguments or order > 1. */
+const gtap_task_table *gtap_table_bfs_split(const int32_t *row_ptr, const int32_t *col,
+                                            int32_t *depth, uint32_t nv, uint32_t order,
+                                            uint32_t edge_split);
+
 /* BFS input preparation (reading R18): depth[v] = INT32_MAX for v != src,
  * depth[src] = 0, asynchronously on `stream`. */
 gtap_status gtap_bfs_init_depth(int32_t *depth, uint32_t nv, int32_t src, void *stream);

@@ -205,15 +205,17 @@ def spmv(row_ptr, col, val, x, y=None, nnz_cut: int = 8192, fanout: int = 16, ro
             rt.close()
 
 
-def bfs(row_ptr, col, src: int, depth=None, rt: Runtime | None = None, stream=None, order: int = 0, **cfg):
+def bfs(row_ptr, col, src: int, depth=None, rt: Runtime | None = None, stream=None, order: int = 0,
+        edge_split: int = 0, **cfg):
     """BFS levels from src (INT32_MAX = unreached) by the paper's frontier-expansion tasks
-    (order 0: LIFO owner pops as in the paper; 1: oldest-first pops, gtap.h gtap_table_bfs_ex)."""
+    (order 0: LIFO owner pops as in the paper; 1: oldest-first pops, gtap.h gtap_table_bfs_ex;
+    edge_split > 0: a vertex with more edges hands pieces of its edge list to bfs_edges tasks)."""
     import torch
     nv = row_ptr.numel() - 1
     if depth is None:
         depth = torch.empty(nv, dtype=torch.int32, device=row_ptr.device)
     rt, own = _runtime(GTAP_WORKER_BLOCK, rt, row_ptr.device.index or 0, cfg)
-    table = Table.bfs(row_ptr, col, depth, order)
+    table = Table.bfs(row_ptr, col, depth, order, edge_split)
     try:
         bfs_init_depth(depth, src, stream)
         rt.spawn_root(table, (src,))

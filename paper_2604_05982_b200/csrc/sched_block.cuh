@@ -43,6 +43,12 @@ struct pop_batch_of { static constexpr int value = 0; };
 template <class T>
 struct pop_batch_of<T, decltype((void)T::kPopBatch, void())> { static constexpr int value = T::kPopBatch; };
 
+// depth of the block's shared-memory free stack (default 256; small blocks packed 32 per SM need less smem)
+template <class T, class = void>
+struct bfstack_of { static constexpr uint32_t value = 256; };
+template <class T>
+struct bfstack_of<T, decltype((void)T::kBlockFreeStack, void())> { static constexpr uint32_t value = T::kBlockFreeStack; };
+
 struct ChildSpec {
     uint32_t fn;
     uint32_t d[kDataWords];
@@ -64,7 +70,7 @@ struct BlockSmem {
     ChildSpec spawns[T::kSpawnCap];
     typename T::Scratch scratch;
     // records of this block's own pool freed here, reused first (no global atomics)
-    uint32_t fstack[256];
+    uint32_t fstack[bfstack_of<T>::value];
     uint32_t nfree;
     // the kept child is dispatched from its staged spec (no record reload)
     ChildSpec kept_spec;
@@ -160,7 +166,7 @@ __device__ __forceinline__ bool block_alloc(const KParams& p, BLeader& L, SM& sm
 template <class SM>
 __device__ __forceinline__ void block_free1(const KParams& p, SM& sm, uint32_t w, uint32_t id) {
     using namespace dev;
-    if ((id >> p.logM) == w && sm.nfree < 256u) {
+    if ((id >> p.logM) == w && sm.nfree < (uint32_t)(sizeof(sm.fstack) / sizeof(sm.fstack[0]))) {
         sm.fstack[sm.nfree++] = id;
         return;
     }

@@ -23,28 +23,31 @@ struct BfsArgs {
     const int32_t* col;
     int32_t* depth;
     uint32_t nv;
-    uint32_t pad;
+    uint32_t split;   // bfs(v) with more than `split` edges spawns bfs_edges pieces of `split` edges (0: never)
 };
-template <uint32_t ORDER>
+// CAP: shared-memory spawn staging (ChildSpecs) and free-stack depth. Blocks of <= 64 threads run the
+// CAP = 128 instantiation (3.3 KB of shared memory: 32 one-warp blocks fit on an SM), larger blocks CAP = 512
+// (a step stages up to 2 x blockDim spawns); gtap_run picks the kernel by block size (launch_bfs below)
+template <uint32_t ORDER, int CAP>
 struct BfsTable {
     static constexpr uint32_t kKind = GTAP_WORKER_BLOCK;
     static constexpr int kMaxChildren = 0;  // dynamic (no taskwait: no join metadata)
     static constexpr bool kTaskwait = false;
-    static constexpr uint32_t kNumFn = 1;
+    static constexpr uint32_t kNumFn = 2;
     static constexpr bool kJoinReduceAdd = false;  // see TaskRec
     static constexpr int kMaxThreads = 1024, kMinBlocks = 1;  // __launch_bounds__
-#ifndef GTAP_BFS_SPAWN_CAP
-#define GTAP_BFS_SPAWN_CAP 512
-#endif
-    static constexpr int kSpawnCap = GTAP_BFS_SPAWN_CAP;
+    static constexpr int kSpawnCap = CAP;
+    static constexpr uint32_t kBlockFreeStack = CAP < 256 ? (uint32_t)CAP : 256u;
 #ifndef GTAP_BFS_U
 #define GTAP_BFS_U 4
 #endif
     static constexpr uint32_t kU = GTAP_BFS_U;       // edges per thread per step
-#ifndef GTAP_BFS_POP_BATCH
-#define GTAP_BFS_POP_BATCH 4
-#endif
+#ifdef GTAP_BFS_POP_BATCH
     static constexpr int kPopBatch = GTAP_BFS_POP_BATCH;  // sched_block.cuh batch pop
+#else
+    // one-warp blocks: 8 (RMAT-22 x 16 sources 4.66 -> 4.46 ms; 6: 4.52); 64-thread blocks: 4 (9.0 ms, 8: 10.8)
+    static constexpr int kPopBatch = CAP < 256 ? 8 : 4;
+#endif
     static constexpr bool kPopOldest = ORDER == 1u;
     static constexpr bool kKeepChild = ORDER == 0u;
 #ifndef GTAP_BFS_TTAS
@@ -57,24 +60,9 @@ struct BfsTable {
         uint32_t unused;
     };
     using Args = BfsArgs;
+    // expand edges [s, e) of a vertex whose depth is dv; uniform over the block
     template <class Ctx>
-    __device__ __forceinline__ static void exec_block(const Args& a, Ctx& ctx, uint32_t fn, uint32_t state,
-                                                      const uint32_t (&d)[kDataWords]) {
-        if (fn != 0u || state != 0u) {
-            if (threadIdx.x == 0) ctx.bad_state();
-            return;
-        }
-        const uint32_t v = d[0];
-        const int32_t dv = dev::ld_relaxed(&a.depth[v]);           // P:1057
-#if GTAP_BFS_SKIP_STALE
-        // d[1] = the depth v had when this task was spawned; a smaller depth now means a later improvement
-        // spawned a newer task for v, which will expand it with that depth: this one has nothing to add
-        if (dv < (int32_t)d[1]) {
-            if (threadIdx.x == 0) ctx.finish_void();
-            return;
-        }
-#endif
-        const int32_t s = __ldg(&a.row_ptr[v]), e = __ldg(&a.row_ptr[v + 1]);  // P:1058-1059
+    __device__ __forceinline__ static void expand(const Args& a, Ctx& ctx, int32_t s, int32_t e, int32_t dv) {
         const int32_t nd = dv + 1;
         const uint32_t bd = blockDim.x;
         // kU edges per thread per step: the kU col loads and then the kU atomicMin are independent,
@@ -111,6 +99,52 @@ struct BfsTable {
                 if (base + (int32_t)step < e) ctx.flush(chunk_every * step);
             }
         }
+    }
+    // fn 0 = bfs(v). fn 1 = bfs_edges(v, lo, hi): edges [lo, hi) of v, spawned by bfs(v) when v
+    // has more than a.split edges (B200 choice, R29: a hub's expansion is cut into pieces other
+    // blocks steal, instead of one block scanning ~1e5 edges on the critical path; same depth writes)
+    template <class Ctx>
+    __device__ __forceinline__ static void exec_block(const Args& a, Ctx& ctx, uint32_t fn, uint32_t state,
+                                                      const uint32_t (&d)[kDataWords]) {
+        if (fn > 1u || state != 0u) {
+            if (threadIdx.x == 0) ctx.bad_state();
+            return;
+        }
+        const uint32_t v = d[0];
+        const int32_t dv = dev::ld_relaxed(&a.depth[v]);           // P:1057
+        if (fn == 1u) {   // a piece of a hub's edge list; dv re-read: it can only have improved since the split
+            expand(a, ctx, (int32_t)d[1], (int32_t)d[2], dv);
+            if (threadIdx.x == 0) ctx.finish_void();
+            return;
+        }
+#if GTAP_BFS_SKIP_STALE
+        // d[1] = the depth v had when this task was spawned; a smaller depth now means a later improvement
+        // spawned a newer task for v, which will expand it with that depth: this one has nothing to add
+        if (dv < (int32_t)d[1]) {
+            if (threadIdx.x == 0) ctx.finish_void();
+            return;
+        }
+#endif
+        const int32_t s = __ldg(&a.row_ptr[v]), e = __ldg(&a.row_ptr[v + 1]);  // P:1058-1059
+        int32_t e0 = e;
+        if (a.split != 0u && (uint32_t)(e - s) > a.split) {
+            // pieces 1.. of [s, e) become bfs_edges tasks; this task scans piece 0
+            const uint32_t sp = a.split;
+            const uint32_t np = (uint32_t)(e - s + (int32_t)sp - 1) / sp;
+            const uint32_t bd = blockDim.x;
+            const uint32_t per = min(bd, (uint32_t)kSpawnCap / 2u);
+            for (uint32_t b = 1; b < np; b += per) {                // uniform
+                const uint32_t i = b + threadIdx.x;
+                if (threadIdx.x < per && i < np) {
+                    const int32_t lo = s + (int32_t)(i * sp);
+                    ctx.spawn(1u, v, (uint32_t)lo, (uint32_t)min(e, lo + (int32_t)sp));
+                }
+                ctx.flush(per);
+            }
+            ctx.flush((uint32_t)kSpawnCap / 2u);   // the edge loop below stages up to half the buffer before its first check
+            e0 = s + (int32_t)sp;
+        }
+        expand(a, ctx, s, e0, dv);
         if (threadIdx.x == 0) ctx.finish_void();
     }
 };
@@ -121,14 +155,37 @@ static int validate_bfs(const gtap_task_table* t, uint32_t fn, const uint32_t* d
     return (fn == 0u && d[0] < a.nv) ? 0 : -1;
 }
 
+static constexpr uint32_t kBfsSmallBlock = 64;   // blocks up to this size run the small-staging kernel
+
+template <uint32_t ORDER>
+cudaError_t launch_bfs(const gtap_task_table* t, const KParams& p, uint32_t grid, uint32_t block, cudaStream_t s) {
+    return block <= kBfsSmallBlock ? launch_block<BfsTable<ORDER, 128>>(t, p, grid, block, s)
+                                   : launch_block<BfsTable<ORDER, 512>>(t, p, grid, block, s);
+}
+template <uint32_t ORDER>
+cudaError_t occupancy_bfs(const gtap_task_table* t, uint32_t block, int* bps, size_t* smem) {
+    return block <= kBfsSmallBlock ? occupancy_block<BfsTable<ORDER, 128>>(t, block, bps, smem)
+                                   : occupancy_block<BfsTable<ORDER, 512>>(t, block, bps, smem);
+}
+template <uint32_t ORDER>
+gtap_task_table* make_bfs(const char* name, const BfsArgs& a) {
+    gtap_task_table* t = make_table<BfsTable<ORDER, 512>>(name, a, &validate_bfs);
+    if (t) { t->launch = &launch_bfs<ORDER>; t->occupancy = &occupancy_bfs<ORDER>; }
+    return t;
+}
+
 }  // namespace gtap
+
+extern "C" const gtap_task_table* gtap_table_bfs_split(const int32_t* row_ptr, const int32_t* col, int32_t* depth,
+                                                       uint32_t nv, uint32_t order, uint32_t edge_split) {
+    if (!row_ptr || !col || !depth || nv == 0 || order > 1u) return nullptr;
+    gtap::BfsArgs a{row_ptr, col, depth, nv, edge_split};
+    return order == 0u ? gtap::make_bfs<0>("bfs", a) : gtap::make_bfs<1>("bfs_fifo", a);
+}
 
 extern "C" const gtap_task_table* gtap_table_bfs_ex(const int32_t* row_ptr, const int32_t* col, int32_t* depth,
                                                     uint32_t nv, uint32_t order) {
-    if (!row_ptr || !col || !depth || nv == 0 || order > 1u) return nullptr;
-    gtap::BfsArgs a{row_ptr, col, depth, nv, 0u};
-    return order == 0u ? gtap::make_table<gtap::BfsTable<0>>("bfs", a, &gtap::validate_bfs)
-                       : gtap::make_table<gtap::BfsTable<1>>("bfs_fifo", a, &gtap::validate_bfs);
+    return gtap_table_bfs_split(row_ptr, col, depth, nv, order, 0u);
 }
 
 extern "C" const gtap_task_table* gtap_table_bfs(const int32_t* row_ptr, const int32_t* col, int32_t* depth,

@@ -67,7 +67,7 @@ EXPORTS = [
     "gtap_spawn_root", "gtap_reset", "gtap_run", "gtap_sync", "gtap_root_result", "gtap_finalize",
     "gtap_geometry", "gtap_table_destroy", "gtap_table_fib", "gtap_table_fib_cutoff", "gtap_table_nqueens", "gtap_table_nqueens_ex", "gtap_table_tree", "gtap_table_mergesort", "gtap_table_mergesort_ex", "gtap_table_cilksort", "gtap_table_cilksort_ex",
     "gtap_table_spmv",
-    "gtap_table_bfs", "gtap_table_bfs_ex", "gtap_bfs_init_depth", "gtap_ubench_atomics", "gtap_ubench_die_probe", "gtap_check_read",
+    "gtap_table_bfs", "gtap_table_bfs_ex", "gtap_table_bfs_split", "gtap_bfs_init_depth", "gtap_ubench_atomics", "gtap_ubench_die_probe", "gtap_check_read",
 ]
 
 _lib = None
@@ -124,6 +124,8 @@ def lib():
     L.gtap_table_bfs.restype = vp
     L.gtap_table_bfs_ex.argtypes = [vp, vp, vp, u32, u32]
     L.gtap_table_bfs_ex.restype = vp
+    L.gtap_table_bfs_split.argtypes = [vp, vp, vp, u32, u32, u32]
+    L.gtap_table_bfs_split.restype = vp
     L.gtap_bfs_init_depth.argtypes = [vp, u32, i32, vp]
     L.gtap_ubench_atomics.argtypes = [vp, u64, u32, u32, u32, u32, vp, P(ctypes.c_float)]
     L.gtap_check_read.argtypes = [vp, P(u64), u32]
@@ -235,11 +237,12 @@ class Table:
                      "spmv", GTAP_WORKER_BLOCK, (row_ptr, col, val, x, y))
 
     @staticmethod
-    def bfs(row_ptr, col, depth, order: int = 0) -> "Table":
-        """order 0: the paper's LIFO owner pops; 1: oldest-first pops (see gtap.h gtap_table_bfs_ex)."""
+    def bfs(row_ptr, col, depth, order: int = 0, edge_split: int = 0) -> "Table":
+        """order 0: the paper's LIFO owner pops; 1: oldest-first pops (see gtap.h gtap_table_bfs_ex);
+        edge_split > 0: hubs' edge lists cut into bfs_edges pieces (gtap.h gtap_table_bfs_split)."""
         _dev_i32(row_ptr, "row_ptr"); _dev_i32(col, "col"); _dev_i32(depth, "depth")
-        return Table(lib().gtap_table_bfs_ex(row_ptr.data_ptr(), col.data_ptr(), depth.data_ptr(), depth.numel(),
-                                             order), "bfs", GTAP_WORKER_BLOCK, (row_ptr, col, depth))
+        return Table(lib().gtap_table_bfs_split(row_ptr.data_ptr(), col.data_ptr(), depth.data_ptr(), depth.numel(),
+                                                order, edge_split), "bfs", GTAP_WORKER_BLOCK, (row_ptr, col, depth))
 
 
 def _dev_i32(t, name):

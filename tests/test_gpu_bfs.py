@@ -45,8 +45,8 @@ def csr_from_edges(nv, edges):
     return torch.tensor(rp, dtype=torch.int32), torch.tensor(col if col else [0], dtype=torch.int32)
 
 
-def check(g, rt, rp, col, src, order=0):
-    depth, st = g.bfs(rp.cuda(), col.cuda(), src, rt=rt, order=order)
+def check(g, rt, rp, col, src, order=0, edge_split=0):
+    depth, st = g.bfs(rp.cuda(), col.cuda(), src, rt=rt, order=order, edge_split=edge_split)
     ref = oracle.bfs(rp, col[: int(rp[-1])] if int(rp[-1]) else col, src)
     assert np.array_equal(depth.cpu().numpy(), ref)
     reached = int((ref != oracle.INT32_MAX).sum())
@@ -150,3 +150,29 @@ def test_die_aware_victims_block_level(g):
         for s in synth.bfs_sources(rp, 2, seed=14):
             check(g, r, rp, col, s)
             check(g, r, rp, col, s, order=1)
+
+
+@pytest.mark.parametrize("order", [0, 1])
+@pytest.mark.parametrize("edge_split", [1, 7, 64, 1000])
+def test_hub_split(g, order, edge_split):
+    """gtap_table_bfs_split: vertices above edge_split edges hand pieces of their edge list to bfs_edges
+    tasks (fn 1); the levels stay exact (stars, complete graph, RMAT hubs, one-edge pieces, ragged last piece)."""
+    with g.Runtime(g.GTAP_WORKER_BLOCK, 0, grid_size=148 * 2, block_size=64, max_tasks_per_worker=1 << 16,
+                   steal_max=32, watchdog_ns=WD) as r:
+        check(g, r, *csr_from_edges(5001, [(0, i) for i in range(1, 5001)]), 0, order, edge_split)   # hub source
+        check(g, r, *csr_from_edges(5001, [(0, i) for i in range(1, 5001)]), 9, order, edge_split)   # via the hub
+        check(g, r, *csr_from_edges(60, list(itertools.combinations(range(60), 2))), 7, order, edge_split)
+        check(g, r, *csr_from_edges(50, [(1, 2), (3, 4)]), 0, order, edge_split)                    # isolated
+        rp, col = synth.rmat_csr(14, 16, seed=edge_split)
+        for s in synth.bfs_sources(rp, 2, seed=edge_split):
+            check(g, r, rp, col, s, order, edge_split)
+
+
+def test_hub_split_full_size(g):
+    """the bench's split + geometry at RMAT-22 (configs[4]), bit-exact levels"""
+    import bench
+    rp, col = synth.rmat_csr(22, 16, seed=3, device="cuda")
+    src = synth.bfs_sources(rp, 2, seed=5)[1]
+    with g.Runtime(g.GTAP_WORKER_BLOCK, 0, watchdog_ns=60_000_000_000, **bench.BFS_CFG) as r:
+        depth, st = g.bfs(rp, col, src, rt=r, order=bench.BFS_ORDER, edge_split=bench.BFS_SPLIT or 2048)
+    assert np.array_equal(depth.cpu().numpy(), oracle.bfs(rp.cpu(), col.cpu(), src))

@@ -126,6 +126,8 @@ struct CheckBuf {
     int32_t* kids;
 };
 
+constexpr uint32_t kPolQueueStay = 1u, kPolDieVictims = 2u;   // KParams::policy bits
+
 // Kernel parameters (by value): geometry + device pointers into one workspace.
 struct KParams {
     uint32_t W;              // workers (warps or blocks)
@@ -137,7 +139,8 @@ struct KParams {
     uint32_t max_child;      // GTAP_MAX_CHILD_TASKS (runtime check)
     uint32_t idle_backoff;   // max idle nanosleep (ns)
     uint32_t nq;             // deques per worker in the workspace (GTAP_NUM_QUEUES, EPAQ)
-    uint32_t qpolicy;        // EPAQ kept-class choice: 0 rotate every cycle, 1 stay while the class has work
+    uint32_t policy;         // kPolQueueStay (EPAQ kept class: stay while the class has work, else rotate every
+                             // cycle) | kPolDieVictims (victim_policy 1: die-aware steal victims, Ctl::vinfo)
     unsigned long long seed;
     unsigned long long watchdog_ns;
     TaskRec* rec;            // W << logM records
@@ -352,21 +355,24 @@ __device__ __forceinline__ uint32_t xorshift32(uint32_t& s) {
     return s;
 }
 
-// a steal victim != w from the random draw r: with victim_policy 1 (vinfo != nullptr) lanes < 24 draw from the
-// workers whose deque line is near the thief's die, the others uniformly
-__device__ __forceinline__ uint32_t pick_victim(uint32_t W, uint32_t w, uint32_t lane, uint32_t r, const Ctl* ctl) {
-    if (lane < 24u) {
+// a steal victim != w from the random draw r: with victim_policy 1 (policy & kPolDieVictims) lanes < 24 draw from
+// the workers whose deque line is near the thief's die, the others uniformly. The uniform draw is a
+// multiply-high range reduction of r (no integer division: idle warps probing for work share the issue slots
+// of the busy warps on their SM; `r % (W - 1)` was 5 % of the mergesort kernel's instructions)
+__device__ __forceinline__ uint32_t pick_victim(uint32_t W, uint32_t w, uint32_t lane, uint32_t r, const Ctl* ctl,
+                                                uint32_t policy) {
+    if ((policy & kPolDieVictims) && lane < 24u) {
         const uint32_t* vi = reinterpret_cast<const uint32_t*>(__ldg(reinterpret_cast<const unsigned long long*>(&ctl->vinfo)));
         if (vi != nullptr) {
             const uint32_t mydie = __ldg(reinterpret_cast<const uint8_t*>(vi) + smid());
             const uint32_t cnt = __ldg(&ctl->vcnt[mydie]);
             if (cnt > 1u) {
-                const uint32_t v = __ldg(vi + 64 + (mydie ? __ldg(&ctl->vcnt[2]) : 0u) + r % cnt);
+                const uint32_t v = __ldg(vi + 64 + (mydie ? __ldg(&ctl->vcnt[2]) : 0u) + __umulhi(r, cnt));
                 return v != w ? v : (v + 1u < W ? v + 1u : 0u);
             }
         }
     }
-    const uint32_t v = r % (W - 1u);
+    const uint32_t v = __umulhi(r, W - 1u);
     return v + (v >= w);
 }
 __device__ __forceinline__ uint32_t lanemask_lt() {

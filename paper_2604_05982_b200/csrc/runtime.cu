@@ -407,7 +407,7 @@ static gtap_status run_impl(gtap_runtime* rt, cudaStream_t s) {
     p.watchdog_ns = rt->cfg.watchdog_ns;
     p.idle_backoff = rt->cfg.idle_backoff_ns;
     p.nq = rt->cfg.num_queues;
-    p.qpolicy = rt->cfg.queue_policy;
+    p.policy = (rt->cfg.queue_policy == 1u ? gtap::kPolQueueStay : 0u) | (rt->vbuf ? gtap::kPolDieVictims : 0u);
     p.rec = reinterpret_cast<gtap::TaskRec*>(rt->ws + rt->L.rec);
     p.ring = reinterpret_cast<uint32_t*>(rt->ws + rt->L.ring);
     p.dq = reinterpret_cast<gtap::DequeMeta*>(rt->ws + rt->L.dq);

@@ -378,7 +378,7 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) block_sched_ker
                 // steal one from the fullest of 32 random victims
                 const uint32_t rounds = L.backoff >= 4096u ? 1u : p.steal_rounds;
                 for (uint32_t round = 0; id == kNone && round < rounds && p.W > 1; ++round) {
-                    const uint32_t v = pick_victim(p.W, w, lane, xorshift32(L.rng), p.ctl);
+                    const uint32_t v = pick_victim(p.W, w, lane, xorshift32(L.rng), p.ctl, p.policy);
                     const unsigned long long sv = ld_relaxed(&p.dq[v].S);
                     uint32_t avail = (uint32_t)(sv >> 32) - (uint32_t)sv;
                     if (avail > Q) avail = 0;

@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
             // a long-idle warp probes once per wake-up (keeps idle L2 traffic off busy workers)
             const uint32_t rounds = backoff >= 4096u ? 1u : p.steal_rounds;
             for (uint32_t round = 0; round < rounds && n == 0; ++round) {
-                const uint32_t v = pick_victim(p.W, w, lane, xorshift32(rng), p.ctl);
+                const uint32_t v = pick_victim(p.W, w, lane, xorshift32(rng), p.ctl, p.policy);
                 const uint32_t vq = (qc + lane) % (uint32_t)NQ;  // EPAQ: round-robin from the own position
                 const uint32_t vd = v * p.nq + vq;
                 const unsigned long long sv = ld_relaxed(&p.dq[vd].S);
@@ -698,7 +698,7 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
             // the kept set holds this cycle's new tasks of that class, so every class -- including
             // continuations, which free records -- is visited every NQ cycles
             uint32_t qk = NQ > 1 ? (qc + 1u) % (uint32_t)NQ : 0u;
-            if (NQ > 1 && p.qpolicy == 1u) {
+            if (NQ > 1 && (p.policy & kPolQueueStay)) {
                 // P:177-178 read literally: stay on the class in use while this cycle produced runnable tasks
                 // of it, else the next class (round robin from it) that did
                 uint32_t has = 0;

@@ -170,6 +170,12 @@ __host__ __device__ constexpr size_t block_extra_bytes() {
     return (sizeof(typename T::BlockExtra) + 127) / 128 * 128;
 }
 
+#ifdef GTAP_CYC_HIST
+// diagnostic build only: per busy cycle, hist[n] += 1 (n = tasks run, 1..32); hist[33] += cycles with n < 32 whose
+// private parts were empty while a public part of the own deque held tasks; hist[34] += those public tasks
+static __device__ unsigned long long gtap_cyc_hist[40];
+#endif
+
 template <class T>
 __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_kernel(KParams p, typename T::Args args) {
     using namespace dev;
@@ -407,6 +413,19 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
         }
         backoff = 32;
         if (lane == 0) { stat(kStCyc, 1); stat(kStInv, n); }
+#ifdef GTAP_CYC_HIST
+        {
+            const unsigned long long s0 = __shfl_sync(0xffffffffu, S_lane, 0);
+            const uint32_t pub = (uint32_t)(s0 >> 32) - (uint32_t)s0;
+            if (lane == 0) {
+                atomicAdd(&gtap_cyc_hist[n], 1ull);
+                if (n < 32u && tail[0] == split[0] && pub > 0u && pub <= Q) {
+                    atomicAdd(&gtap_cyc_hist[33], 1ull);
+                    atomicAdd(&gtap_cyc_hist[34], (unsigned long long)pub);
+                }
+            }
+        }
+#endif
 
         // ================= (2) execute, one task per lane =================
         Out o;

@@ -129,3 +129,12 @@ extern "C" const gtap_task_table* gtap_table_fib_cutoff(int32_t cutoff, uint32_t
     gtap::FibCutoffTable<1>::Args a{(uint32_t)cutoff};
     return gtap::make_table<gtap::FibCutoffTable<1>>("fib_cutoff", a, &gtap::validate_fib);
 }
+
+#ifdef GTAP_CYC_HIST
+extern "C" int gtap_cyc_hist_read(unsigned long long* h) {   // diagnostic build only (sched_thread.cuh)
+    cudaMemcpyFromSymbol(h, gtap::gtap_cyc_hist, sizeof(unsigned long long) * 40);
+    unsigned long long z[40] = {};
+    cudaMemcpyToSymbol(gtap::gtap_cyc_hist, z, sizeof(z));
+    return 0;
+}
+#endif

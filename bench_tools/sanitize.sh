@@ -7,7 +7,7 @@ TAG=${1:-r02}
 OUT=gpurun_out/${TAG}_sanitize.txt
 : > $OUT
 for tool in memcheck racecheck synccheck; do
-  for t in ${TABLES:-fib fibdie ms ms0 cs nq spmv bfs bfs1 tree}; do
+  for t in ${TABLES:-fib fibdie ms ms0 cs nq spmv bfs bfs1 bfs32 tree}; do
     log=gpurun_out/${TAG}_san_${tool}_${t}.log
     timeout -s KILL 900 compute-sanitizer --tool $tool --kernel-name regex=sched_kernel --print-limit 20 \
         python bench_tools/sanitize_probe.py $t > $log 2>&1

@@ -1,6 +1,6 @@
 """Small runs of the hot tables for compute-sanitizer (memcheck / racecheck / synccheck / initcheck).
 
-usage: compute-sanitizer --tool <tool> python bench_tools/sanitize_probe.py <fib|ms|ms0|spmv|bfs|bfs1|tree|cs|nq|fibdie>
+usage: compute-sanitizer --tool <tool> python bench_tools/sanitize_probe.py <fib|ms|ms0|spmv|bfs|bfs1|bfs32|tree|cs|nq|fibdie>
 
 Each run is checked against the oracle so a sanitizer-clean run is also a correct one; sizes are small
 (the sanitizers slow every memory access down by 10-100x) but span several workers, steals and, for
@@ -48,6 +48,12 @@ elif what == "spmv":
     y64, _ = oracle.spmv(rp, col, val, x)
     e = np.abs(y.cpu().numpy().astype(np.float64) - y64) / np.maximum(np.abs(y64), 1e-30)
     assert np.all((y64 == 0) | (e <= 1e-5))
+elif what == "bfs32":   # the bench's shape: one-warp blocks (128-entry staging kernel), hub pieces, oldest-first pops
+    rp, col = synth.rmat_csr(12, 16, seed=4)
+    src = synth.bfs_sources(rp, 1, seed=4)[0]
+    depth, st = g.bfs(rp.cuda(), col.cuda(), src, grid_size=148 * 4, block_size=32, max_tasks_per_worker=1 << 13,
+                      steal_max=32, watchdog_ns=WD, order=1, edge_split=64)
+    assert np.array_equal(depth.cpu().numpy(), oracle.bfs(rp, col, src))
 elif what in ("bfs", "bfs1"):
     rp, col = synth.rmat_csr(10, 16, seed=4)
     src = synth.bfs_sources(rp, 1, seed=4)[0]

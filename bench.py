@@ -289,7 +289,7 @@ def bench_mergesort(args, ws, rank, dev):
     # sorts them and copies them out. Pipelined (3 buffers): step i+1's H2D (stream s_in) and step
     # i-1's D2H (stream s_out) overlap step i's sort (compute stream); every step's copies are inside
     # the timed region, which spans all steps. A serial variant is reported beside it.
-    NB = 3
+    NB = int(os.environ.get("GTAP_E2E_NB", 3))
     host_in = [pristine.cpu().pin_memory() for _ in range(NB)]
     host_out = [torch.empty_like(host_in[0]).pin_memory() for _ in range(NB)]
     kb = [keys] + [torch.empty_like(keys) for _ in range(NB - 1)]
@@ -313,7 +313,13 @@ def bench_mergesort(args, ws, rank, dev):
     e2e_serial_ms = _max_over_ranks(statistics.mean(e2e_ms), ws, dev)
     s_in, s_out, sc = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
     tables = [table] + [g.Table.mergesort(kb[j], scratch, MS_CUTOFF, MS_MERGE_MODE) for j in range(1, NB)]
-    ksteps = max(6, args.steps)
+    # two runtimes (two workspaces) used alternately: a run is enqueued on the compute stream behind the previous
+    # one without the host first waiting for it (gtap_sync of a runtime only before its next-but-one reuse), so
+    # the GPU never idles on a host round trip between consecutive sorts
+    rts = [rt, g.Runtime(g.GTAP_WORKER_THREAD, dev.index, **MS_CFG)]
+    # a stream of 32 sorts (or --steps if more): the pipeline fill (first H2D) and drain (last D2H), ~2 ms each,
+    # are paid once per stream (10 steps: 1.9 ms per step; 40: 1.58; 100: 1.49 -- transfer-bound steady state)
+    ksteps = int(os.environ.get("GTAP_E2E_STEPS", max(32, args.steps)))
     ev_in = [torch.cuda.Event() for _ in range(NB)]
     ev_sorted = [torch.cuda.Event() for _ in range(NB)]
     ev_out = [torch.cuda.Event() for _ in range(NB)]
@@ -332,18 +338,20 @@ def bench_mergesort(args, ws, rank, dev):
                 ev_in[bi].record(s_in)
         if i >= 1:
             bj = (i - 1) % NB
+            r_ = rts[(i - 1) % 2]
             sc.wait_event(ev_in[bj])
-            if i >= 2:
-                rt.sync()
-            rt.reset(sc)
-            rt.spawn_root(tables[bj], (0, n))
-            rt.run(sc)
+            if i >= 3:
+                r_.sync()
+            r_.reset(sc)
+            r_.spawn_root(tables[bj], (0, n))
+            r_.run(sc)
             ev_sorted[bj].record(sc)
             with torch.cuda.stream(s_out):
                 s_out.wait_event(ev_sorted[bj])
                 host_out[bj].copy_(kb[bj], non_blocking=True)
                 ev_out[bj].record(s_out)
-    rt.sync()
+    for r_ in rts[:min(2, ksteps)]:
+        r_.sync()
     sc.wait_stream(s_out)
     t_b.record(sc)
     torch.cuda.synchronize()
@@ -352,6 +360,7 @@ def bench_mergesort(args, ws, rank, dev):
         bool(torch.all(host_out[0][1:] >= host_out[0][:-1]).item())
     for t in tables[1:]:
         t.close()
+    rts[1].close()
     st = stats[-1]
     algo_bytes = 8.0 * n * (1 + _ms_levels(n, MS_CUTOFF))  # read+write per key per pass
     pk, src = peaks()
@@ -360,7 +369,7 @@ def bench_mergesort(args, ws, rank, dev):
         value=ws * n / (ms * 1e-3) / 1e6, ms_per_step=ms, wall_ms_per_step=wall * 1e3 / args.steps,
         e2e=dict(value=ws * n / (e2e_pipe_ms * 1e-3) / 1e6, unit=UNIT, h2d_bytes_per_step=4 * n,
                  d2h_bytes_per_step=4 * n, ms_per_step=e2e_pipe_ms,
-                 mode="pipelined (3 buffers: H2D / sort / D2H of consecutive steps overlap)",
+                 mode="pipelined (3 buffers: H2D / sort / D2H of consecutive steps overlap; two runtimes alternate so the next sort is queued before the previous one ends)",
                  steps=ksteps, correct=pipe_ok,
                  serial=dict(value=ws * n / (e2e_serial_ms * 1e-3) / 1e6, ms_per_step=e2e_serial_ms)),
         roofline=dict(bound="hbm", achieved=achieved, peak=pk["hbm_gbs"], unit="GB/s",

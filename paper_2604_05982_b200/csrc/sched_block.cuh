@@ -49,6 +49,13 @@ struct bfstack_of { static constexpr uint32_t value = 256; };
 template <class T>
 struct bfstack_of<T, decltype((void)T::kBlockFreeStack, void())> { static constexpr uint32_t value = T::kBlockFreeStack; };
 
+// multi-task cycles (tables without taskwait): a cycle runs up to kMultiTask tasks of a popped batch at once,
+// T::exec_multi (e.g. BFS on one-warp blocks: groups of lanes expand several small vertices side by side)
+template <class T, class = void>
+struct multi_task_of { static constexpr int value = 1; };
+template <class T>
+struct multi_task_of<T, decltype((void)T::kMultiTask, void())> { static constexpr int value = T::kMultiTask; };
+
 struct ChildSpec {
     uint32_t fn;
     uint32_t d[kDataWords];
@@ -79,6 +86,11 @@ struct BlockSmem {
     uint4 bq_h[pop_batch_of<T>::value > 0 ? pop_batch_of<T>::value : 1];
     uint4 bq_d[pop_batch_of<T>::value > 0 ? pop_batch_of<T>::value : 1];
     uint32_t bq_id[pop_batch_of<T>::value > 0 ? pop_batch_of<T>::value : 1];
+    // multi-task cycle: the cycle's tasks (mt_n of them; task 0 is also in fn/state/d above)
+    uint32_t mt_n;
+    uint32_t mt_fn[multi_task_of<T>::value];   // fn | state << 8
+    uint32_t mt_id[multi_task_of<T>::value];
+    uint32_t mt_d[multi_task_of<T>::value][kDataWords];
 };
 
 // Leader-side (warp 0) persistent state.
@@ -266,6 +278,8 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) block_sched_ker
     __shared__ BlockSmem<T> sm;
     constexpr int kPB = pop_batch_of<T>::value;
     static_assert(kPB <= 32, "one lane per batched pop");
+    constexpr int kMT = multi_task_of<T>::value;
+    static_assert(kMT == 1 || (!T::kTaskwait && kPB >= kMT), "multi-task cycles: tables without taskwait, batch pops");
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const uint32_t w = blockIdx.x;
     if (w >= p.W) return;
@@ -448,10 +462,30 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) block_sched_ker
                     }
                     sm.kept_fresh = 0;
                     GTAP_CK(ck_dispatch(p, id, sm.state));
+                    if constexpr (kMT > 1) {
+                        // more tasks of the popped batch run in this cycle (one ring / record round trip for all)
+                        uint32_t k = 1;
+                        sm.mt_fn[0] = sm.fn | (sm.state << 8); sm.mt_id[0] = id;   // fn | state << 8
+                        sm.mt_d[0][0] = sm.d[0]; sm.mt_d[0][1] = sm.d[1]; sm.mt_d[0][2] = sm.d[2]; sm.mt_d[0][3] = sm.d[3];
+                        if (from_bq >= 0) {
+                            while (k < (uint32_t)kMT && L.bq_i < L.bq_n) {
+                                const uint32_t b = L.bq_i++;
+                                const uint4 h = sm.bq_h[b];
+                                const uint4 dv = sm.bq_d[b];
+                                sm.mt_fn[k] = meta_fn(h.z) | (meta_state(h.z) << 8); sm.mt_id[k] = sm.bq_id[b];
+                                sm.mt_d[k][0] = dv.x; sm.mt_d[k][1] = dv.y; sm.mt_d[k][2] = dv.z; sm.mt_d[k][3] = dv.w;
+                                GTAP_CK(ck_dispatch(p, sm.bq_id[b], 0u));
+                                ++k;
+                            }
+                        }
+                        sm.mt_n = k;
+                        L.st[ST_INVOC] += k - 1u;
+                    }
                     sm.nspawn = 0; sm.action = 0; sm.has_result = 0; sm.err = 0;
                     ++L.st[ST_CYCLES];
                     ++L.st[ST_INVOC];
                 }
+                if constexpr (kMT > 1) L.bq_i = __shfl_sync(0xffffffffu, L.bq_i, 0);
                 L.backoff = 64;
             } else {
                 if (lane == 0) ++L.st[ST_IDLE];
@@ -484,7 +518,9 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) block_sched_ker
 #ifdef GTAP_TRACE
         const unsigned long long tr0 = dev::globaltimer();
 #endif
-        {
+        if constexpr (kMT > 1) {
+            T::exec_multi(args, ctx, sm.mt_n, sm.mt_fn, sm.mt_d);
+        } else {
             const uint32_t d[kDataWords] = {sm.d[0], sm.d[1], sm.d[2], sm.d[3]};
             T::exec_block(args, ctx, sm.fn, sm.state, d);
         }
@@ -508,14 +544,15 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) block_sched_ker
                 // +children must reach the counter before they are published; this task's -1 may be
                 // deferred (the counter then only stays positive longer): fold it into the +children
                 // when there are children, else batch it locally (flushed every 64 tasks or when idle)
+                const uint32_t nfin = kMT > 1 ? sm.mt_n : 1u;
                 if (staged) {
-                    const long long delta = (long long)staged - 1ll - (long long)L.local_dec;
+                    const long long delta = (long long)staged - (long long)nfin - (long long)L.local_dec;
                     L.local_dec = 0;
                     if (delta > 0) red_add_relaxed(reinterpret_cast<unsigned long long*>(&p.ctl->outstanding),
                                                    (unsigned long long)delta);
                     else if (delta < 0 && atom_add_acq_rel(&p.ctl->outstanding, delta) == -delta)
                         st_release(&p.ctl->done, 1u);
-                } else if (++L.local_dec >= 64u) {
+                } else if ((L.local_dec += nfin) >= 64u) {
                     const long long dec = (long long)L.local_dec;
                     L.local_dec = 0;
                     if (atom_add_acq_rel(&p.ctl->outstanding, -dec) == dec) st_release(&p.ctl->done, 1u);
@@ -546,6 +583,14 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) block_sched_ker
                         st_relaxed(reinterpret_cast<int32_t*>(&p.rec[parent].d[2 + sm.ord]), sm.result);
                     GTAP_CK(if (lane == 0) ck_free(p, my));
                     if (lane == 0) block_free1(p, sm, w, my);
+                    if constexpr (kMT > 1) {
+                        if (lane == 0) {
+                            for (uint32_t k = 1; k < sm.mt_n; ++k) {
+                                GTAP_CK(ck_free(p, sm.mt_id[k]));
+                                block_free1(p, sm, w, sm.mt_id[k]);
+                            }
+                        }
+                    }
                     __syncwarp();
                     uint32_t resume = kNone;
                     if (lane == 0) {

@@ -28,7 +28,7 @@ struct BfsArgs {
 // CAP: shared-memory spawn staging (ChildSpecs) and free-stack depth. Blocks of <= 64 threads run the
 // CAP = 128 instantiation (3.3 KB of shared memory: 32 one-warp blocks fit on an SM), larger blocks CAP = 512
 // (a step stages up to 2 x blockDim spawns); gtap_run picks the kernel by block size (launch_bfs below)
-template <uint32_t ORDER, int CAP>
+template <uint32_t ORDER, int CAP, int MT = 1>
 struct BfsTable {
     static constexpr uint32_t kKind = GTAP_WORKER_BLOCK;
     static constexpr int kMaxChildren = 0;  // dynamic (no taskwait: no join metadata)
@@ -42,6 +42,12 @@ struct BfsTable {
 #define GTAP_BFS_U 4
 #endif
     static constexpr uint32_t kU = GTAP_BFS_U;       // edges per thread per step
+    // MT > 1 (one-warp blocks): a cycle expands up to MT tasks of a popped batch side by side, 32 / MT lanes each
+    static constexpr int kMultiTask = MT;
+#ifndef GTAP_BFS_MT_EDGES
+#define GTAP_BFS_MT_EDGES 64
+#endif
+    static constexpr uint32_t kMtEdges = GTAP_BFS_MT_EDGES;   // edges per task scanned by its lane group
 #ifdef GTAP_BFS_POP_BATCH
     static constexpr int kPopBatch = GTAP_BFS_POP_BATCH;  // sched_block.cuh batch pop
 #else
@@ -147,6 +153,86 @@ struct BfsTable {
         expand(a, ctx, s, e0, dv);
         if (threadIdx.x == 0) ctx.finish_void();
     }
+    // MT tasks of a popped batch in one cycle of a one-warp block (B200 choice, DESIGN.md §5 "Multi-task cycles"):
+    // group g = lanes [g G, g G + G), G = 32 / MT, expands task g's first kMtEdges edges (its hub pieces spawned
+    // first); what is left of larger tasks is then expanded by the whole warp, task by task. Same depth writes as
+    // MT single-task cycles, with one dependent chain of round trips for all of them.
+    template <class Ctx>
+    __device__ __forceinline__ static void exec_multi(const Args& a, Ctx& ctx, uint32_t cnt, const uint32_t (&fs)[MT],
+                                                      const uint32_t (&dd)[MT][kDataWords]) {
+        static_assert(MT > 1 && 32 % MT == 0, "lane groups of one warp");
+        constexpr uint32_t G = 32u / (uint32_t)MT;
+        constexpr uint32_t kUa = 2;                         // edges per lane per group step
+        static_assert(32u * kUa <= (uint32_t)CAP / 2u, "a group step stages at most half the buffer");
+        const uint32_t lane = threadIdx.x & 31u;
+        bool bad = false;
+#pragma unroll
+        for (int k = 0; k < MT; ++k)
+            if ((uint32_t)k < cnt && ((fs[k] & 0xFFu) > 1u || (fs[k] >> 8) != 0u)) bad = true;
+        if (bad) {
+            if (lane == 0) ctx.bad_state();
+            return;
+        }
+        const uint32_t g = lane / G, gl = lane % G;
+        const bool act = g < cnt;
+        const uint32_t fn = act ? (fs[g] & 0xFFu) : 0u;
+        const uint32_t v = act ? dd[g][0] : 0u;
+        int32_t dv = 0, s = 0, e = 0;
+        if (act) {
+            dv = dev::ld_relaxed(&a.depth[v]);
+            if (fn == 1u) { s = (int32_t)dd[g][1]; e = (int32_t)dd[g][2]; }
+            else { s = __ldg(&a.row_ptr[v]); e = __ldg(&a.row_ptr[v + 1]); }
+        }
+        // hub pieces (R29), G per group per round
+        if (a.split != 0u) {
+            const uint32_t sp = a.split;
+            const uint32_t np = (act && fn == 0u && (uint32_t)(e - s) > sp) ? (uint32_t)(e - s + (int32_t)sp - 1) / sp : 1u;
+            const uint32_t mx = __reduce_max_sync(0xffffffffu, np);
+            if (mx > 1u) {
+                for (uint32_t b = 1; b < mx; b += G) {
+                    const uint32_t i = b + gl;
+                    if (i < np) {
+                        const int32_t lo = s + (int32_t)(i * sp);
+                        ctx.spawn(1u, v, (uint32_t)lo, (uint32_t)min(e, lo + (int32_t)sp));
+                    }
+                    ctx.flush(32u);
+                }
+                ctx.flush((uint32_t)CAP / 2u);
+                if (np > 1u) e = s + (int32_t)sp;
+            }
+        }
+        const int32_t nd = dv + 1;
+        // phase A: every group its task's first kMtEdges edges
+        const int32_t ea = min(e, s + (int32_t)kMtEdges);
+        const uint32_t steps = (uint32_t)__reduce_max_sync(0xffffffffu, (uint32_t)max(0, ea - s)) ;
+        for (uint32_t base = 0; base < steps; base += G * kUa) {
+            int32_t u[kUa];
+#pragma unroll
+            for (uint32_t j = 0; j < kUa; ++j) {
+                const int32_t i = s + (int32_t)(base + gl + j * G);
+                u[j] = (act && i < ea) ? __ldg(&a.col[i]) : -1;
+            }
+            int32_t cur[kUa];
+#pragma unroll
+            for (uint32_t j = 0; j < kUa; ++j) cur[j] = u[j] >= 0 ? dev::ld_relaxed(&a.depth[u[j]]) : nd;
+#pragma unroll
+            for (uint32_t j = 0; j < kUa; ++j) {
+                const int32_t old = cur[j] > nd ? atomicMin(&a.depth[u[j]], nd) : nd;
+                if (old > nd) ctx.spawn(0u, (uint32_t)u[j], (uint32_t)nd);
+            }
+            ctx.flush(32u * kUa);
+        }
+        // phase B: the rest of larger tasks, whole warp, one task at a time
+        const uint32_t rest = __ballot_sync(0xffffffffu, act && gl == 0u && ea < e);
+        for (uint32_t k = 0; k < (uint32_t)MT; ++k) {
+            if (!((rest >> (k * G)) & 1u)) continue;            // uniform
+            const int32_t sk = __shfl_sync(0xffffffffu, ea, k * G), ek = __shfl_sync(0xffffffffu, e, k * G);
+            const int32_t dk = __shfl_sync(0xffffffffu, dv, k * G);
+            expand(a, ctx, sk, ek, dk);
+            ctx.flush((uint32_t)CAP / 2u);
+        }
+        if (lane == 0) ctx.finish_void();
+    }
 };
 
 static int validate_bfs(const gtap_task_table* t, uint32_t fn, const uint32_t* d) {
@@ -157,13 +243,18 @@ static int validate_bfs(const gtap_task_table* t, uint32_t fn, const uint32_t* d
 
 static constexpr uint32_t kBfsSmallBlock = 64;   // blocks up to this size run the small-staging kernel
 
+#ifndef GTAP_BFS_MT
+#define GTAP_BFS_MT 4   // tasks per cycle of a one-warp block (1: one task per cycle)
+#endif
 template <uint32_t ORDER>
 cudaError_t launch_bfs(const gtap_task_table* t, const KParams& p, uint32_t grid, uint32_t block, cudaStream_t s) {
+    if (block == 32u) return launch_block<BfsTable<ORDER, 128, GTAP_BFS_MT>>(t, p, grid, block, s);
     return block <= kBfsSmallBlock ? launch_block<BfsTable<ORDER, 128>>(t, p, grid, block, s)
                                    : launch_block<BfsTable<ORDER, 512>>(t, p, grid, block, s);
 }
 template <uint32_t ORDER>
 cudaError_t occupancy_bfs(const gtap_task_table* t, uint32_t block, int* bps, size_t* smem) {
+    if (block == 32u) return occupancy_block<BfsTable<ORDER, 128, GTAP_BFS_MT>>(t, block, bps, smem);
     return block <= kBfsSmallBlock ? occupancy_block<BfsTable<ORDER, 128>>(t, block, bps, smem)
                                    : occupancy_block<BfsTable<ORDER, 512>>(t, block, bps, smem);
 }

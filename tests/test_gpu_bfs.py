@@ -152,12 +152,14 @@ def test_die_aware_victims_block_level(g):
             check(g, r, rp, col, s, order=1)
 
 
+@pytest.mark.parametrize("block", [32, 64])
 @pytest.mark.parametrize("order", [0, 1])
 @pytest.mark.parametrize("edge_split", [1, 7, 64, 1000])
-def test_hub_split(g, order, edge_split):
+def test_hub_split(g, order, edge_split, block):
     """gtap_table_bfs_split: vertices above edge_split edges hand pieces of their edge list to bfs_edges
-    tasks (fn 1); the levels stay exact (stars, complete graph, RMAT hubs, one-edge pieces, ragged last piece)."""
-    with g.Runtime(g.GTAP_WORKER_BLOCK, 0, grid_size=148 * 2, block_size=64, max_tasks_per_worker=1 << 16,
+    tasks (fn 1); the levels stay exact (stars, complete graph, RMAT hubs, one-edge pieces, ragged last piece).
+    Block 32 runs the one-warp kernel with multi-task cycles (lane groups), block 64 one task per cycle."""
+    with g.Runtime(g.GTAP_WORKER_BLOCK, 0, grid_size=148 * 2, block_size=block, max_tasks_per_worker=1 << 16,
                    steal_max=32, watchdog_ns=WD) as r:
         check(g, r, *csr_from_edges(5001, [(0, i) for i in range(1, 5001)]), 0, order, edge_split)   # hub source
         check(g, r, *csr_from_edges(5001, [(0, i) for i in range(1, 5001)]), 9, order, edge_split)   # via the hub
@@ -176,3 +178,22 @@ def test_hub_split_full_size(g):
     with g.Runtime(g.GTAP_WORKER_BLOCK, 0, watchdog_ns=60_000_000_000, **bench.BFS_CFG) as r:
         depth, st = g.bfs(rp, col, src, rt=r, order=bench.BFS_ORDER, edge_split=bench.BFS_SPLIT or 2048)
     assert np.array_equal(depth.cpu().numpy(), oracle.bfs(rp.cpu(), col.cpu(), src))
+
+
+@pytest.mark.parametrize("order", [0, 1])
+def test_one_warp_blocks(g, order):
+    """one-warp blocks (multi-task cycles) without hub splitting: special graphs, random graphs, RMAT"""
+    with g.Runtime(g.GTAP_WORKER_BLOCK, 0, grid_size=148 * 4, block_size=32, max_tasks_per_worker=1 << 15,
+                   steal_max=32, watchdog_ns=WD) as r:
+        n = 300
+        check(g, r, *csr_from_edges(n, [(i, i + 1) for i in range(n - 1)]), 0, order)
+        check(g, r, *csr_from_edges(n, [(0, i) for i in range(1, n)]), 5, order)
+        check(g, r, *csr_from_edges(60, list(itertools.combinations(range(60), 2))), 7, order)
+        for seed in range(4):
+            rng = np.random.default_rng(100 + seed)
+            nv = int(rng.integers(2, 400))
+            edges = [tuple(rng.integers(0, nv, 2).tolist()) for _ in range(int(rng.integers(0, 6 * nv)))]
+            check(g, r, *csr_from_edges(nv, edges), int(rng.integers(0, nv)), order)
+        rp, col = synth.rmat_csr(16, 16, seed=31)
+        for s in synth.bfs_sources(rp, 2, seed=31):
+            check(g, r, rp, col, s, order)

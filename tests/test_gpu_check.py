@@ -130,14 +130,17 @@ if "bfs" in what:
     rp, col = synth.rmat_csr(14, 16, seed=4)
     src = synth.bfs_sources(rp, 1, seed=4)[0]
     lv = oracle.bfs(rp, col, src)
-    for cfg in (dict(grid_size=148, block_size=64, max_tasks_per_worker=1 << 16, steal_max=32),
-                dict(grid_size=148 * 4, block_size=64, max_tasks_per_worker=1 << 16),
-                dict(grid_size=1, block_size=32, max_tasks_per_worker=1 << 18)):
-        def runb(rt):
-            return g.bfs(rp.cuda(), col.cuda(), src, rt=rt)
-        ck, st = checked(f"bfs_{cfg['grid_size']}_{cfg.get('steal_max', 1)}", B, cfg, runb,
-                         lambda depth, st: bool(np.array_equal(depth.cpu().numpy(), lv)))
-        res[f"bfs_{cfg['grid_size']}_{cfg.get('steal_max', 1)}"]["ok"] &= ck["outstanding"] == 0
+    for cfg, kw in ((dict(grid_size=148, block_size=64, max_tasks_per_worker=1 << 16, steal_max=32), {}),
+                    (dict(grid_size=148 * 4, block_size=64, max_tasks_per_worker=1 << 16), {}),
+                    (dict(grid_size=1, block_size=32, max_tasks_per_worker=1 << 18), {}),
+                    # the bench's shape: one-warp blocks (multi-task cycles), oldest-first pops, hub pieces
+                    (dict(grid_size=148 * 8, block_size=32, max_tasks_per_worker=1 << 15, steal_max=32),
+                     dict(order=1, edge_split=64))):
+        def runb(rt, kw=kw):
+            return g.bfs(rp.cuda(), col.cuda(), src, rt=rt, **kw)
+        name = f"bfs_{cfg['grid_size']}_{cfg.get('steal_max', 1)}"
+        ck, st = checked(name, B, cfg, runb, lambda depth, st: bool(np.array_equal(depth.cpu().numpy(), lv)))
+        res[name]["ok"] &= ck["outstanding"] == 0
 if "spmv" in what:
     rp, col, val, x = synth.powerlaw_csr(1 << 13, seed=2)
     y64, _ = oracle.spmv(rp, col, val, x)

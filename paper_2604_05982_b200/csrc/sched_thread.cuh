@@ -110,6 +110,14 @@ struct gen_children_of { static constexpr bool value = false; };
 template <class T>
 struct gen_children_of<T, decltype((void)T::kGenChildren, void())> { static constexpr bool value = T::kGenChildren; };
 
+// a word idle warps poll while they probe steal victims (e.g. mergesort's GPU-wide assist board: nonzero while a
+// slot is open); lane 31 reads it instead of a victim's deque word, and a failed steal round that saw it set goes
+// to T::help_idle at once
+template <class T, class = void>
+struct idle_word_of { static constexpr bool value = false; };
+template <class T>
+struct idle_word_of<T, decltype((void)T::kIdleWord, void())> { static constexpr bool value = T::kIdleWord; };
+
 template <class T, class = void>
 struct assist_of { static constexpr bool value = false; };
 template <class T>
@@ -377,18 +385,31 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
         if (n == 0 && p.W > 1) {
             // a long-idle warp probes once per wake-up (keeps idle L2 traffic off busy workers)
             const uint32_t rounds = backoff >= 4096u ? 1u : p.steal_rounds;
+            bool board = false;
             for (uint32_t round = 0; round < rounds && n == 0; ++round) {
                 const uint32_t v = pick_victim(p.W, w, lane, xorshift32(rng), p.ctl, p.policy);
                 const uint32_t vq = (qc + lane) % (uint32_t)NQ;  // EPAQ: round-robin from the own position
                 const uint32_t vd = v * p.nq + vq;
-                const unsigned long long sv = ld_relaxed(&p.dq[vd].S);
-                uint32_t avail = (uint32_t)(sv >> 32) - (uint32_t)sv;
-                if (avail > Q) avail = 0;
+                uint32_t avail = 0, polled = 0;
+                if (idle_word_of<T>::value && lane == 31u) {
+                    if constexpr (idle_word_of<T>::value) {
+                        const uint32_t* pw = T::idle_word(args);
+                        polled = pw ? ld_relaxed(pw) : 0u;
+                    }
+                } else {
+                    const unsigned long long sv = ld_relaxed(&p.dq[vd].S);
+                    avail = (uint32_t)(sv >> 32) - (uint32_t)sv;
+                    if (avail > Q) avail = 0;
+                }
                 // warp arg-max over (avail, lane)
                 uint32_t best = (min(avail, (1u << 26)) << 5) | lane;
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
-                if ((best >> 5) == 0) { if (lane == 0) stat(kStSfail, 1); continue; }
+                if ((best >> 5) == 0) {
+                    if (lane == 0) stat(kStSfail, 1);
+                    if (idle_word_of<T>::value && __shfl_sync(0xffffffffu, polled, 31) != 0u) { board = true; break; }
+                    continue;
+                }
                 const uint32_t bl = best & 31u;
                 const uint32_t vdq = __shfl_sync(0xffffffffu, vd, bl);
                 const uint32_t vqq = __shfl_sync(0xffffffffu, vq, bl);
@@ -428,6 +449,9 @@ __global__ void __launch_bounds__(T::kMaxThreads, T::kMinBlocks) thread_sched_ke
                 } else if (lane == 0) {
                     stat(kStSfail, 1);
                 }
+            }
+            if constexpr (assist_of<T>::value && idle_word_of<T>::value) {
+                if (n == 0 && board && T::help_idle(args, lane, bx)) { backoff = 32; continue; }
             }
         }
         done_seen = __shfl_sync(0xffffffffu, done_seen, 31);

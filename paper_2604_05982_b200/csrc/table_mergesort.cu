@@ -1087,6 +1087,12 @@ struct MergesortTable {
         return true;
     }
 
+    // scheduler hook: idle warps poll the board's open-slot count while probing steal victims (sched_thread.cuh
+    // idle_word_of), so a slot opened during a steal round is seen one round trip later
+    static constexpr bool kIdleWord = MODE == 1u;
+    __device__ __forceinline__ static const uint32_t* idle_word(const Args& a) {
+        return a.gb ? &a.gb->open : nullptr;
+    }
     // scheduler hook, idle path (all 32 lanes): help an open GPU-wide assist
     __device__ __forceinline__ static bool help_idle(const Args& a, uint32_t lane, WarpAssistHolder* H) {
         if (a.gb == nullptr) return false;

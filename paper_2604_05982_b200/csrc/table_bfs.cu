@@ -42,8 +42,6 @@ struct BfsTable {
 #define GTAP_BFS_U 4
 #endif
     static constexpr uint32_t kU = GTAP_BFS_U;       // edges per thread per step
-    // MT > 1 (one-warp blocks): a cycle expands up to MT tasks of a popped batch side by side, 32 / MT lanes each
-    static constexpr int kMultiTask = MT;
 #ifndef GTAP_BFS_MT_EDGES
 #define GTAP_BFS_MT_EDGES 64
 #endif
@@ -54,6 +52,8 @@ struct BfsTable {
     // one-warp blocks: 8 (RMAT-22 x 16 sources 4.66 -> 4.46 ms; 6: 4.52); 64-thread blocks: 4 (9.0 ms, 8: 10.8)
     static constexpr int kPopBatch = CAP < 256 ? 8 : 4;
 #endif
+    // MT > 1 (one-warp blocks): a cycle expands up to MT tasks of a popped batch side by side, 32 / MT lanes each
+    static constexpr int kMultiTask = kPopBatch >= MT ? MT : 1;   // the batch supplies the extra tasks
     static constexpr bool kPopOldest = ORDER == 1u;
     static constexpr bool kKeepChild = ORDER == 0u;
 #ifndef GTAP_BFS_TTAS

@@ -60,11 +60,12 @@ for name, n in (("ms", 1 << 18), ("ms_ragged", 100003), ("ms_big", 1 << 22), ("m
 if "bfs" in what:
     rp, col = synth.rmat_csr(14, 16, seed=4)
     src = synth.bfs_sources(rp, 1, seed=4)[0]
-    for grid, block in ((148, 64), (1, 32)):
+    for grid, block, split in ((148, 64, 0), (1, 32, 0), (148 * 4, 32, 64)):
         for order in (0, 1):
             depth, st = g.bfs(rp.cuda(), col.cuda(), src, grid_size=grid, block_size=block,
-                              max_tasks_per_worker=1 << 16, steal_max=32, watchdog_ns=60_000_000_000, order=order)
-            res[f"bfs{grid}_{order}"] = bool(np.array_equal(depth.cpu().numpy(), oracle.bfs(rp, col, src)))
+                              max_tasks_per_worker=1 << 16, steal_max=32, watchdog_ns=60_000_000_000, order=order,
+                              edge_split=split)
+            res[f"bfs{grid}_{block}_{order}"] = bool(np.array_equal(depth.cpu().numpy(), oracle.bfs(rp, col, src)))
 if "cs" in what:
     keys = synth.keys_int32(300007, seed=5).numpy()
     d = torch.from_numpy(keys).cuda()

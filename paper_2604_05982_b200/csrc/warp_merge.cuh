@@ -27,7 +27,7 @@ namespace gtap {
 namespace wm3 {
 
 #ifndef GTAP_MS_VT
-#define GTAP_MS_VT 15
+#define GTAP_MS_VT 13   // 9 / 11 / 13 / 15 / 17 / 19: 1.337 / 1.29 / 1.26 / 1.29 / 1.30 / 1.30 ms at 2^24
 #endif
 constexpr int VT = GTAP_MS_VT;                // outputs per lane per tile (odd: conflict-free output buffer)
 constexpr int T = 32 * VT;                    // outputs per tile (a multiple of 4)

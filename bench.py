@@ -78,7 +78,9 @@ BFS_SOURCES = 16         # 16 seeded sources, median
 # one-warp blocks, 32 per SM (the 128-entry staging kernel: 3.3 KB of shared memory per block): 2368 x 64 -> 4736 x 32
 # with hub splitting 7.8 -> 4.8 ms per source (bench_tools/bfs_ab.sh); batch steals (the paper's block-level steal
 # takes 1): 33 -> 8.6 ms at 2368 x 64
-BFS_CFG = dict(grid_size=148 * 32, block_size=32, max_tasks_per_worker=1 << 17, idle_backoff_ns=4096,
+# 2^16 records per block (12 GB of workspace; 2^15 / 2^16 / 2^17 measured equal, 3.85 / 3.86 / 3.84 ms, and 2^15
+# already holds every source's local frontiers: bench_tools/bfs_pool_sweep.sh)
+BFS_CFG = dict(grid_size=148 * 32, block_size=32, max_tasks_per_worker=1 << 16, idle_backoff_ns=4096,
                steal_max=32)
 BFS_ORDER = 1            # oldest-first owner pops (gtap_table_bfs_ex): 9.4 -> 8.4 ms per source
 BFS_SPLIT = 1024         # hub edge lists cut into bfs_edges pieces of this many edges (gtap_table_bfs_split; 0 = off)

@@ -32,7 +32,7 @@ struct SpmvTable {
     static constexpr int kMaxThreads = GTAP_SPMV_MAXT, kMinBlocks = GTAP_SPMV_MINB;  // __launch_bounds__ (prod[] holds 8 x 256)
     static constexpr int kSpawnCap = 32;
 #ifndef GTAP_SPMV_PER
-#define GTAP_SPMV_PER 16   // with 256-thread blocks: 4 K non-zeros per chunk (8 x 128: 0.868 ms; 16 x 256: 0.80 ms at the bench shape)
+#define GTAP_SPMV_PER 24   // with 256-thread blocks: 6 K non-zeros per chunk (12 / 16 / 20 / 24 / 28 / 32: 0.74 / 0.71 / - / 0.69 / 0.74 / 0.73 ms at the bench shape; 20 and 28 spill)
 #endif
     static constexpr int kPer = GTAP_SPMV_PER;  // non-zeros per thread per chunk
     static constexpr int kMaxBlock = 256;   // prod[] sized for blocks up to 256 threads

@@ -864,7 +864,11 @@ struct MergesortTable {
     // placement hint: subtrees whose merges take the TMA path are spread over warps (never two
     // in one warp's kept set, where they would share issue slots and the block's merge slot)
     static constexpr bool kHasHeavy = true;
-    __device__ __forceinline__ static bool heavy(uint32_t, const uint32_t* d) { return d[1] - d[0] >= kTmaMin; }
+#ifndef GTAP_MS_HEAVY_MIN
+#define GTAP_MS_HEAVY_MIN 8192   // warp mode placement hint (4096 / 8192 / 16384 / 32768: 1.255 / 1.26 / 1.31 / 1.31 ms)
+#endif
+    static constexpr uint32_t kHeavyMin = MODE == 1u ? GTAP_MS_HEAVY_MIN : kTmaMin;
+    __device__ __forceinline__ static bool heavy(uint32_t, const uint32_t* d) { return d[1] - d[0] >= kHeavyMin; }
     __device__ __forceinline__ static bool heavy_parent(uint32_t, const uint32_t* d) {
 #if GTAP_MS_KEEP_GLOBAL
         // a resumed parent whose merge goes to the GPU-wide board stays in the kept set: every idle warp
@@ -872,7 +876,7 @@ struct MergesortTable {
         // critical path (join -> slot open)
         if (MODE == 1u && 2u * (d[1] - d[0]) >= kGlobalAssistMin) return false;
 #endif
-        return 2u * (d[1] - d[0]) >= kTmaMin;
+        return 2u * (d[1] - d[0]) >= kHeavyMin;
     }
     static constexpr int kMaxThreads = 128;                    // __launch_bounds__
     static constexpr int kMinBlocks = MODE == 1u ? GTAP_MS_WARP_MINB : 4;

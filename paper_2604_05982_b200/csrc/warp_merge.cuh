@@ -18,7 +18,7 @@
 // WM3Tiles::par) before the tile; every chunk issued is waited for before the call returns, and the
 // bulk stores are complete (and fenced to the generic proxy) before it returns.
 // Requires 16-B aligned src / dst arrays whose length n4 is a multiple of 4 (bulk granularity);
-// chunks are 1 KB-aligned in the array and may read keys outside [a0, m) / [b0, r) (never used).
+// chunks are C-key (2 KB) aligned in the array and may read keys outside [a0, m) / [b0, r) (never used).
 #pragma once
 #include <climits>
 #include <cstdint>
@@ -31,9 +31,12 @@ namespace wm3 {
 #endif
 constexpr int VT = GTAP_MS_VT;                // outputs per lane per tile (odd: conflict-free output buffer)
 constexpr int T = 32 * VT;                    // outputs per tile (a multiple of 4)
-constexpr int C = 256;                        // keys per bulk chunk (1 KB)
+#ifndef GTAP_MS_C
+#define GTAP_MS_C 512   // 256 x 4 / 512 x 2 / 128 x 8 (keys per chunk x chunks per ring): 1.26 / 1.24 / 1.31-1.34 ms
+#endif
+constexpr int C = GTAP_MS_C;                  // keys per bulk chunk (2 KB)
 #ifndef GTAP_MS_NS
-#define GTAP_MS_NS 4
+#define GTAP_MS_NS 2
 #endif
 constexpr int NS = GTAP_MS_NS;                // chunks per ring
 constexpr int R = C * NS;                     // keys per ring

@@ -7,7 +7,8 @@ oracle: the options are alternative implementations of the same task bodies / sc
 
 * GTAP_FSTACK=1, GTAP_FIB_FSTACK=1: a one-entry own free stack, so nearly every surplus free takes
   the overflow path to the home free ring (fib, trees, Cilksort, N-Queens).
-* GTAP_MS_VT=23, GTAP_MS_BITONIC_MAX=1024: the bulk-copy merge core with 736-key tiles (default 480) and bitonic merges up to 1024 keys (default 512).
+* GTAP_MS_VT=15, GTAP_MS_C=256, GTAP_MS_NS=4, GTAP_MS_BITONIC_MAX=1024: the bulk-copy merge core with 480-key tiles
+  fed by 1 KB chunks x 4 (default: 416-key tiles, 2 KB chunks x 2) and bitonic merges up to 1024 keys (default 512).
 * GTAP_CS_KARY=0: Cilksort's plain binary split search.
 * GTAP_BFS_POP_BATCH=0 / 32: single pops and the largest batch pop of the block-level leader;
   GTAP_BFS_SKIP_STALE=1: a task whose vertex improved since its spawn returns at once (measured slower);
@@ -92,13 +93,13 @@ def _probe(lib, what):
 
 @pytest.mark.parametrize("defines,what", [
     (("GTAP_FSTACK=1", "GTAP_FIB_FSTACK=1"), "fib tree nq cs"),
-    (("GTAP_MS_VT=23", "GTAP_MS_BITONIC_MAX=1024"), "ms"),
+    (("GTAP_MS_VT=15", "GTAP_MS_C=256", "GTAP_MS_NS=4", "GTAP_MS_BITONIC_MAX=1024"), "ms"),
     (("GTAP_CS_KARY=0",), "cs"),
     (("GTAP_BFS_POP_BATCH=0",), "bfs"),
     (("GTAP_BFS_POP_BATCH=32",), "bfs"),
     (("GTAP_BFS_SKIP_STALE=1",), "bfs"),
     (("GTAP_BFS_TTAS=0",), "bfs"),
-], ids=["fstack1", "ms_vt23_bitonic1024", "cs_binary_split", "bfs_pop1",
+], ids=["fstack1", "ms_vt15_c256_bitonic1024", "cs_binary_split", "bfs_pop1",
         "bfs_pop32", "bfs_skip_stale", "bfs_atomic_always"])
 def test_variant_parity(cuda_device, defines, what):
     lib = _variant(defines)

@@ -128,6 +128,28 @@ def test_full_size_config1(g, mode):
     assert (st.tasks, st.invocations) == (tasks, inv) == (262143, 393214)
 
 
+def test_full_size_forest_c5b(g):
+    """configs[4] C5b per GPU: a forest of 16 independent 2^20-key arrays (seeds 1000 + k, as bench_forest), one root per array, in
+    ONE launch at the bench's launch configuration (bench.bench_forest); every array against the oracle."""
+    import torch
+
+    import bench
+    k, n = bench.FOREST_WEAK_PER_GPU, bench.FOREST_EACH
+    arrs = [synth.keys_int32(n, seed=1000 + j) for j in range(k)]
+    d = torch.cat(arrs).cuda()
+    segs = [(j * n, (j + 1) * n) for j in range(k)]
+    with g.Runtime(g.GTAP_WORKER_THREAD, 0, watchdog_ns=60_000_000_000, **dict(bench.MS_CFG, max_roots=k)) as r:
+        st = g.mergesort_forest_(d, segs, cutoff=bench.MS_CUTOFF, merge_mode=bench.MS_MERGE_MODE, rt=r)
+    out = d.cpu().numpy()
+    tasks = inv = 0
+    for j, (l, rr) in enumerate(segs):
+        ref, t, i = oracle.mergesort(arrs[j].numpy(), bench.MS_CUTOFF)
+        assert np.array_equal(out[l:rr], ref), j
+        tasks += t
+        inv += i
+    assert (st.tasks, st.invocations) == (tasks, inv)
+
+
 def test_forest_tma_segments(g, mode):
     import torch
     # segment lengths multiple of 4 but not of the 512-key chunk: TMA merges with partial chunks,

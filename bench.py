@@ -69,7 +69,8 @@ SPMV_NNZ_CUT = 65536
 SPMV_FANOUT = 4          # a root range above the cut splits into 4 (fanout 32 made ~3 K-nnz slivers)
 SPMV_PARTS = 148 * 4     # forest: one nnz-balanced root per worker (fn part(k, R), reading R20)
 SPMV_CFG = dict(grid_size=148 * 4, block_size=256, max_tasks_per_worker=1024, max_roots=SPMV_PARTS)
-CS_CFG = dict(grid_size=0, block_size=128, max_tasks_per_worker=4096, idle_backoff_ns=1024)
+# steals of up to 16 tasks (32 / 16 / 8 / 4: 4.20 / 3.95 / 4.02 / 4.57 ms at 2^24: bench_tools/cs_cfg_sweep.py steal)
+CS_CFG = dict(grid_size=0, block_size=128, max_tasks_per_worker=4096, idle_backoff_ns=1024, steal_max=16)
 NQ_N = 16
 NQ_CUTOFF = 7
 NQ_CFG = dict(grid_size=0, block_size=128, max_tasks_per_worker=4096)
